@@ -1,0 +1,192 @@
+/*
+ * rgdbek.h — C ABI of the B200-native RGDBEK hot path (arXiv 2509.19267).
+ *
+ * The operation: solve A x = b, A in R^{m x n}, b in R^m (PAPER.md P:38-41,
+ * eq:Ax=b) with the randomized greedy double-block extended Kaczmarz sweep of
+ * Algorithm 1, in the pseudoinverse-free form BASELINE.json's
+ * north_star prescribes (reading R1):
+ *
+ *   x_0 = 0, z_0 = b
+ *   for k = 0, 1, ...
+ *     s = A^T z_k;  eps^z_j = s_j^2 / ||A_(j)||^2
+ *     U_k = the k_c indices with the smallest Philox exponential keys
+ *           -ln(u_j)/eps^z_j  (sampling "n eta columns using P(j_k)")
+ *     zeta = s on U_k;  w = A zeta;  z_{k+1} = z_k - (||zeta||^2/||w||^2) w
+ *     r = b - z_{k+1} - A x_k;  eps^x_i = r_i^2 / ||A^(i)||^2
+ *     J_k = the k_r smallest row keys ("m eta rows using P(i_k)")
+ *     xi = r on J_k;  v = A^T xi;  x_{k+1} = x_k + (||xi||^2/||v||^2) v
+ *   stop on RSE = ||A x - b||^2/||b||^2 <= tol, or on
+ *   ||x - x*||/||x*|| <= tol (BASELINE.json metric), or on the iteration cap.
+ *
+ * with k_c = max(1, floor(eta n + 1/2)) and k_r = max(1, floor(eta m + 1/2))
+ * clamped to the number of positive scores, and the Philox4x32-10 stream
+ * u(seed, k, step, index) defined in DESIGN.md §2 (readings R2-R6).
+ *
+ * Conventions
+ *  - All floating point is IEEE binary64 (double); indices are int32 (column
+ *    and row indices) and int64 (CSR row offsets, sizes, iteration counts).
+ *  - Pointers passed IN may be host or device (CUDA unified addressing; torch
+ *    CUDA tensors pass data_ptr()).  create() deep-copies A and b into device
+ *    memory owned by the handle; the library never keeps a caller pointer.
+ *    get_*() write into caller buffers (host or device).
+ *  - Every call returns an rgdbek_status; negative = error.  The message of
+ *    the last error is rgdbek_last_error(handle) (or (NULL) for create
+ *    failures, thread-local).  CUDA / NCCL errors are sticky: once one is
+ *    seen every later call on that handle returns the same code.
+ *  - A handle is not thread-safe; distinct handles are independent.  All work
+ *    runs on options.stream (or a library stream); calls that return results
+ *    synchronise that stream before returning.
+ *  - Multi-GPU: each rank creates its handle with the GLOBAL m, n, its own
+ *    contiguous global row range [row_begin, row_end) and its local rows of A
+ *    and b (column indices global), plus an ncclComm_t in options.nccl_comm.
+ *    x (n) is replicated; z (local rows) is sharded.  Results are identical
+ *    on every rank.
+ *  - No CPU fallback exists: without a usable sm_100 GPU create() fails with
+ *    RGDBEK_E_CUDA.
+ */
+#ifndef RGDBEK_H_
+#define RGDBEK_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RGDBEK_ABI_VERSION 1
+
+typedef struct rgdbek_ctx* rgdbek_handle;
+
+typedef enum {
+  RGDBEK_OK = 0,
+  RGDBEK_E_ARG = -1,        /* NULL pointer, eta not in (0,1), tol <= 0, n_iter < 0, ...      */
+  RGDBEK_E_DIM = -2,        /* m, n < 1, row range outside [0, m), inconsistent lengths         */
+  RGDBEK_E_CSR = -3,        /* row_ptr[0] != 0, non-monotone, row_ptr[m] != nnz, col >= n or
+                               < 0, columns not strictly increasing within a row               */
+  RGDBEK_E_ZERO_RHS = -4,   /* ||b|| == 0: RSE undefined                            */
+  RGDBEK_E_NONFINITE = -5,  /* NaN / Inf in A or b                                              */
+  RGDBEK_E_STATE = -6,      /* e.g. STOP_REL_ERR without rgdbek_set_reference                   */
+  RGDBEK_E_CUDA = -7,       /* CUDA runtime error or no sm_100 device (sticky)                  */
+  RGDBEK_E_NCCL = -8,       /* NCCL error (sticky)                                              */
+  RGDBEK_E_OOM = -9,        /* device allocation failed                                         */
+  RGDBEK_E_INTERNAL = -10   /* a device self-check failed (e.g. block size mismatch)            */
+} rgdbek_status;
+
+typedef enum {              /* rgdbek_result.outcome (SPEC exit codes 0/2/3)                    */
+  RGDBEK_CONVERGED = 0,
+  RGDBEK_MAX_ITER = 2,
+  RGDBEK_STALLED = 3        /* both blocks empty (no positive score mass) before the stop test */
+} rgdbek_outcome;
+
+typedef enum {
+  RGDBEK_STOP_RSE = 0,      /* ||A x - b||^2 / ||b||^2 <= tol (the paper's RSE)      */
+  RGDBEK_STOP_REL_ERR = 1,  /* ||x - x*|| / ||x*|| <= tol, x* from rgdbek_set_reference          */
+  RGDBEK_STOP_NONE = 2      /* iterate to the cap                                               */
+} rgdbek_stop;
+
+typedef struct {
+  double  eta;              /* block fraction, in (0,1); default 0.5                    */
+  int32_t stop;             /* rgdbek_stop used by rgdbek_solve; default RGDBEK_STOP_RSE        */
+  int32_t device;           /* CUDA ordinal; default 0                                          */
+  void*   stream;           /* cudaStream_t to run on; NULL = a library-owned stream           */
+  void*   nccl_comm;        /* ncclComm_t; NULL = single GPU                                    */
+  int64_t row_begin;        /* this rank's first global row; -1 (default) = 0                   */
+  int64_t row_end;          /* one past this rank's last global row; -1 (default) = m          */
+  int32_t symmetric;        /* 1 = caller asserts A == A^T (square CSR); the CSR then also
+                               serves as the transposed copy.  Verified at create.             */
+  int32_t trace_capacity;   /* per-iteration records kept on device (ring); default 4096       */
+} rgdbek_options;
+
+typedef struct {
+  int32_t outcome;          /* rgdbek_outcome                                                   */
+  int32_t pad_;
+  int64_t iters;            /* total iterations k of the returned iterate x_k                   */
+  double  rse;              /* RSE(x_k) = ||A x_k - b||^2 / ||b||^2                              */
+  double  rel_err;          /* ||x_k - x*|| / ||x*|| (NaN without a reference)                  */
+  double  seconds;          /* device time of the call (CUDA events on the handle's stream)    */
+} rgdbek_result;
+
+typedef struct {            /* what iteration k produced (trace ring, rgdbek_get_trace)         */
+  int64_t  k;
+  int64_t  kp;              /* |U_k|                                                            */
+  uint64_t hash_u;          /* sum of splitmix64(j) over j in U_k, mod 2^64                     */
+  double   Z;               /* ||zeta||^2                                                       */
+  double   W;               /* ||A zeta||^2                                                     */
+  int64_t  kpp;             /* |J_k|                                                            */
+  uint64_t hash_j;          /* sum of splitmix64(i) over GLOBAL rows i in J_k                   */
+  double   X;               /* ||xi||^2                                                         */
+  double   V;               /* ||A^T xi||^2                                                     */
+  double   rse;             /* RSE(x_{k+1})                                                     */
+} rgdbek_trace_record;
+
+int32_t       rgdbek_abi_version(void);
+void          rgdbek_options_default(rgdbek_options* opts);
+
+/* Create from CSR rows [row_begin, row_end) of A (m_local = row_end - row_begin rows):
+ * row_ptr_local[m_local+1] (int64, row_ptr_local[0] == 0), col_idx[nnz_local] (int32, global
+ * column ids, strictly increasing within each row), val[nnz_local], b_local[m_local]. */
+rgdbek_status rgdbek_create_csr(rgdbek_handle* out, int64_t m, int64_t n, int64_t nnz_local,
+                                const int64_t* row_ptr_local, const int32_t* col_idx,
+                                const double* val, const double* b_local,
+                                const rgdbek_options* opts);
+
+/* Create from a dense row-major block of rows: A_local[i*lda + j], lda >= n. */
+rgdbek_status rgdbek_create_dense(rgdbek_handle* out, int64_t m, int64_t n,
+                                  const double* A_local, int64_t lda, const double* b_local,
+                                  const rgdbek_options* opts);
+
+/* x = 0, z = b, k = 0, sampler seed = seed. */
+rgdbek_status rgdbek_reset(rgdbek_handle h, uint64_t seed);
+
+/* Exactly n_iter more iterations from the current state, no stop test.
+ * result->rse is RSE of the final iterate. */
+rgdbek_status rgdbek_step(rgdbek_handle h, int64_t n_iter, rgdbek_result* result);
+
+/* reset(seed), then iterate until the stop test (options.stop / rgdbek_set_stop) holds
+ * after an iteration, both blocks are empty (STALLED), or max_iter iterations ran. */
+rgdbek_status rgdbek_solve(rgdbek_handle h, double tol, int64_t max_iter, uint64_t seed,
+                           rgdbek_result* result);
+
+rgdbek_status rgdbek_set_stop(rgdbek_handle h, int32_t stop);
+rgdbek_status rgdbek_set_reference(rgdbek_handle h, const double* xstar /* n values */);
+
+rgdbek_status rgdbek_get_x(rgdbek_handle h, double* out_n);
+rgdbek_status rgdbek_get_z(rgdbek_handle h, double* out_local_m);
+
+/* Blocks of the last completed iteration (k-1).  U / J may be NULL; else they receive the
+ * sorted indices (U: columns, n_u values; J: GLOBAL rows of this rank, n_j values). */
+rgdbek_status rgdbek_get_blocks(rgdbek_handle h, int64_t* n_u, uint64_t* hash_u, int32_t* U,
+                                int64_t* n_j, uint64_t* hash_j, int32_t* J);
+
+/* Copies up to max_records trace records of iterations [max(0, k - cap), k) in order. */
+rgdbek_status rgdbek_get_trace(rgdbek_handle h, rgdbek_trace_record* out, int64_t max_records,
+                               int64_t* n_out);
+
+/* Resume from a saved state: x (n), z_local, iteration k (the seed stays). */
+rgdbek_status rgdbek_set_state(rgdbek_handle h, const double* x, const double* z_local, int64_t k);
+
+/* Timing hook for the bench: enqueue `reps` launches of one hot kernel on the handle's stream
+ * (kernel 0 = pass T [A^T z, A^T xi], 1 = pass N [A zeta, A x]).  Clobbers the iteration
+ * state: call rgdbek_reset afterwards.  bytes_per_launch receives the algorithmic bytes. */
+rgdbek_status rgdbek_launch_kernel(rgdbek_handle h, int32_t kernel, int32_t reps,
+                                   double* bytes_per_launch);
+
+/* Kernels launched per iteration body (for the bench's gpu_launches count). */
+rgdbek_status rgdbek_launches_per_iteration(rgdbek_handle h, int64_t* out);
+
+/* The cudaStream_t the handle runs on (for events / synchronisation). */
+void*         rgdbek_stream(rgdbek_handle h);
+
+/* NCCL bootstrap helpers (rank 0 makes the id; it is broadcast by the caller). */
+rgdbek_status rgdbek_nccl_unique_id(void* out_128_bytes);
+rgdbek_status rgdbek_nccl_comm_init(void** comm_out, int32_t nranks, int32_t rank,
+                                    const void* id_128_bytes, int32_t device);
+rgdbek_status rgdbek_nccl_comm_destroy(void* comm);
+
+const char*   rgdbek_last_error(rgdbek_handle h);
+void          rgdbek_destroy(rgdbek_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RGDBEK_H_ */

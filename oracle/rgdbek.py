@@ -107,13 +107,20 @@ def sample_keys(eps, seed, k, step):
     u = uniforms(np.arange(len(eps)), k, step, seed)
     kappa = np.full(len(eps), np.inf)
     pos = eps > 0
-    kappa[pos] = -np.log(u[pos]) / eps[pos]
+    with np.errstate(over="ignore"):            # an overflow to +inf is the IEEE result
+        kappa[pos] = -np.log(u[pos]) / eps[pos]
     return kappa
 
 
-def select_block(kappa, kk):
-    """Indices of the kk smallest (kappa_j, j) pairs, sorted (reading R4: lower index wins ties)."""
-    order = np.lexsort((np.arange(len(kappa)), kappa))
+def select_block(kappa, kk, eligible=None):
+    """Indices of the kk smallest (kappa_j, j) pairs, sorted (reading R4: lower index wins ties).
+
+    Indices with eps == 0 (``eligible`` False) are never taken before eligible
+    ones (reading R6); the caller clamps kk to the eligible count.
+    """
+    n = len(kappa)
+    never = np.zeros(n, dtype=bool) if eligible is None else ~np.asarray(eligible)
+    order = np.lexsort((np.arange(n), kappa, never))
     return np.sort(order[:kk])
 
 
@@ -171,7 +178,7 @@ class Oracle:
         eps = scores(s, self.gamma)                        # eps^z
         kappa = sample_keys(eps, seed, self.k, 0)
         kp = min(self.kc, int(np.count_nonzero(eps > 0)))  # clamp (reading R6)
-        U = select_block(kappa, kp)
+        U = select_block(kappa, kp, eps > 0)
         zeta = np.zeros(self.n)
         zeta[U] = s[U]
         Z = float(s[U] @ s[U])
@@ -188,7 +195,7 @@ class Oracle:
         eps = scores(r, self.rho)                          # eps^x
         kappa = sample_keys(eps, seed, self.k, 1)
         kpp = min(self.kr, int(np.count_nonzero(eps > 0)))
-        J = select_block(kappa, kpp)
+        J = select_block(kappa, kpp, eps > 0)
         xi = np.zeros(self.m)
         xi[J] = r[J]
         X = float(r[J] @ r[J])

@@ -1,0 +1,930 @@
+// runtime.cu — host runtime and the C ABI of include/rgdbek.h.
+//
+// One handle = one GPU (one rank).  create() copies A, b to HBM, validates,
+// computes the norm caches rho and gamma, builds the transposed
+// (CSC) copy for pass T, and captures ONE iteration body into a CUDA graph
+// driven by a device-side WHILE node, so solve()/step() run entirely on the
+// GPU: the host crosses the device boundary only at entry and exit.
+#include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+using namespace rg;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct rgdbek_ctx {
+  // problem
+  long long m = 0, n = 0, m_loc = 0, row0 = 0, nnz = 0;
+  bool dense = false, symmetric = false;
+  double eta = 0.5;
+  int stop_mode = RGDBEK_STOP_RSE;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  void* nccl = nullptr;
+  long long trace_cap = 0;
+  bool has_ref = false;
+  // dense A
+  double* A = nullptr;
+  long long lda = 0;
+  int R = 0, P = 0, tiles = 0;
+  // CSR (+ CSC)
+  long long* rp = nullptr;
+  int* ci = nullptr;
+  double* cv = nullptr;
+  long long* cp = nullptr;   // CSC col_ptr (or == rp when symmetric)
+  int* ri = nullptr;
+  double* rv = nullptr;
+  int vecN = 8, vecT = 8;
+  // vectors
+  double *b = nullptr, *rho = nullptr, *gamma = nullptr;
+  double *x = nullptr, *s = nullptr, *v = nullptr, *zeta = nullptr, *xstar = nullptr;
+  double *z = nullptr, *w = nullptr, *ax = nullptr, *r = nullptr, *xi = nullptr;
+  unsigned long long *keys_n = nullptr, *keys_m = nullptr;
+  unsigned char* selmask_n = nullptr;   // [2][n]   parity of k
+  unsigned char* selmask_m = nullptr;   // [2][m_loc]
+  double* part = nullptr;               // dense pass T partials [P][2][n]
+  double* bpart = nullptr;              // per-block partials [4 * MAXBLK]
+  unsigned int* hist = nullptr;         // [NBINS]
+  Cand* cand = nullptr;                 // [CAND_CAP]
+  TraceRec* trace = nullptr;
+  Scal* st = nullptr;
+  Scal* st_host = nullptr;              // pinned mirror
+  double bnorm2 = 0.0;
+  // graph
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t body_graph = nullptr;
+  cudaGraphExec_t body_exec = nullptr;  // fallback when conditional nodes are unavailable
+  bool use_cond = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  long long launches_per_iter = 0;
+  // errors
+  int sticky = 0;
+  std::string err;
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+rgdbek_status set_err(rgdbek_ctx* h, rgdbek_status code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h) {
+    h->err = buf;
+    if (code == RGDBEK_E_CUDA || code == RGDBEK_E_NCCL) h->sticky = code;
+  } else {
+    g_create_error = buf;
+  }
+  return code;
+}
+
+#define CK(h, call)                                                                        \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return set_err((h), e_ == cudaErrorMemoryAllocation ? RGDBEK_E_OOM : RGDBEK_E_CUDA, \
+                     "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__,   \
+                     __LINE__);                                                            \
+  } while (0)
+
+template <typename T>
+rgdbek_status dalloc(rgdbek_ctx* h, T** p, size_t count) {
+  void* q = nullptr;
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess)
+    return set_err(h, RGDBEK_E_OOM, "cudaMalloc(%zu bytes) failed: %s", bytes,
+                   cudaGetErrorString(e));
+  h->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  return RGDBEK_OK;
+}
+
+#define TRY(x)                      \
+  do {                              \
+    rgdbek_status s_ = (x);         \
+    if (s_ != RGDBEK_OK) return s_; \
+  } while (0)
+
+inline int nblocks(long long work, int per_block, int cap) {
+  long long b = (work + per_block - 1) / per_block;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (int)b;
+}
+
+// ---------------------------------------------------------------------------
+// Setup kernels (one-time; a0 of SURVEY §8(a))
+// ---------------------------------------------------------------------------
+__global__ void k_check_finite(const double* a, long long count, int* flag) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    if (!isfinite(a[i])) atomicOr(flag, 1);
+}
+
+__global__ void k_validate_csr(const long long* rp, const int* ci, long long m_loc, long long n,
+                               long long nnz, int* flag) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m_loc;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long p0 = rp[i], p1 = rp[i + 1];
+    if (p1 < p0 || p0 < 0 || p1 > nnz) { atomicOr(flag, 2); continue; }
+    for (long long p = p0; p < p1; ++p) {
+      const int c = ci[p];
+      if (c < 0 || c >= n) { atomicOr(flag, 4); break; }
+      if (p > p0 && ci[p - 1] >= c) { atomicOr(flag, 8); break; }
+    }
+  }
+}
+
+// rho_i = sum_p val_p^2 over row i of a CSR (also gamma from the CSC: same kernel)
+__global__ void k_csr_sqnorm(const long long* rp, const double* val, long long rows, double* out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+       i += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (long long p = rp[i]; p < rp[i + 1]; ++p) acc = fma(val[p], val[p], acc);
+    out[i] = acc;
+  }
+}
+
+__global__ void k_dense_rownorm(const double* A, long long lda, long long m, long long n,
+                                double* out) {
+  const int lane = threadIdx.x & 31;
+  const long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long i = wid; i < m; i += nw) {
+    double acc = 0.0;
+    for (long long j = lane; j < n; j += 32) acc = fma(A[i * lda + j], A[i * lda + j], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) out[i] = acc;
+  }
+}
+
+__global__ void k_dense_colnorm(const double* A, long long lda, long long m, long long n,
+                                double* out) {
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (long long i = 0; i < m; ++i) acc = fma(A[i * lda + j], A[i * lda + j], acc);
+    out[j] = acc;
+  }
+}
+
+__global__ void k_expand_rows(const long long* rp, long long rows, int* row_of) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+       i += (long long)gridDim.x * blockDim.x)
+    for (long long p = rp[i]; p < rp[i + 1]; ++p) row_of[p] = (int)i;
+}
+
+__global__ void k_iota(int* a, long long count) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    a[i] = (int)i;
+}
+
+__global__ void k_col_count(const int* ci, long long nnz, long long* cnt /* n+1, zeroed */) {
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+       p += (long long)gridDim.x * blockDim.x)
+    atomicAdd((unsigned long long*)&cnt[ci[p] + 1], 1ull);
+}
+
+__global__ void k_gather_csc(const int* perm, const int* row_of, const double* val, long long nnz,
+                             int* ri, double* rv) {
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int q = perm[p];
+    ri[p] = row_of[q];
+    rv[p] = val[q];
+  }
+}
+
+__global__ void k_compare(const long long* a, const long long* b, long long n1, const int* c,
+                          const int* d, const double* e, const double* f, long long n2,
+                          int* flag) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n1 || i < n2;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (i < n1 && a[i] != b[i]) atomicOr(flag, 1);
+    if (i < n2 && (c[i] != d[i] || e[i] != f[i])) atomicOr(flag, 1);
+  }
+}
+
+__global__ void k_selmask_to_list(const unsigned char* mask, long long count, long long base,
+                                  int* out, unsigned long long* pos) {
+  // order is restored on the host (std::sort) — this is a debug/readout path only
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    if (mask[i]) out[atomicAdd(pos, 1ull)] = (int)(base + i);
+}
+
+int pick_vec(double avg) {
+  int v = 2;
+  while (v < 32 && v < avg) v <<= 1;
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// The iteration body (enqueued once for capture; also used by the fallback loop)
+// ---------------------------------------------------------------------------
+template <int VEC, int MODE>
+void launch_csr(rgdbek_ctx* h, const long long* ptr, const int* idx, const double* val,
+                long long nrows, const double* in1, const double* in2, const double* b,
+                double* o1, double* o2, cudaGraphConditionalHandle) {
+  const int rows_per_block = NT / VEC;
+  const int grid = nblocks(nrows, rows_per_block, MAXBLK);
+  k_csr_dual<VEC, MODE><<<grid, NT, 0, h->stream>>>(ptr, idx, val, (int)nrows, in1, in2, b, o1,
+                                                    o2, h->st, h->trace, h->bpart);
+}
+
+template <int MODE>
+void launch_csr_vec(rgdbek_ctx* h, int vec, const long long* ptr, const int* idx,
+                    const double* val, long long nrows, const double* in1, const double* in2,
+                    const double* b, double* o1, double* o2) {
+  cudaGraphConditionalHandle c{};
+  switch (vec) {
+    case 2: launch_csr<2, MODE>(h, ptr, idx, val, nrows, in1, in2, b, o1, o2, c); break;
+    case 4: launch_csr<4, MODE>(h, ptr, idx, val, nrows, in1, in2, b, o1, o2, c); break;
+    case 8: launch_csr<8, MODE>(h, ptr, idx, val, nrows, in1, in2, b, o1, o2, c); break;
+    case 16: launch_csr<16, MODE>(h, ptr, idx, val, nrows, in1, in2, b, o1, o2, c); break;
+    default: launch_csr<32, MODE>(h, ptr, idx, val, nrows, in1, in2, b, o1, o2, c); break;
+  }
+}
+
+constexpr int PT_TPB = 128;   // dense pass T: threads per block (2 columns each)
+
+void launch_passT(rgdbek_ctx* h) {
+  if (h->dense) {
+    dim3 grid(h->tiles, h->P);
+    k_dense_passT<PT_TPB><<<grid, PT_TPB, 2 * h->R * sizeof(double), h->stream>>>(
+        h->A, h->lda, (int)h->m_loc, (int)h->n, h->R, h->z, h->xi, h->part, h->st);
+  } else {
+    launch_csr_vec<1>(h, h->vecT, h->cp, h->ri, h->rv, h->n, h->z, h->xi, nullptr, h->s, h->v);
+  }
+}
+
+void launch_passN(rgdbek_ctx* h) {
+  if (h->dense) {
+    constexpr int ROWS = 2;
+    const long long groups = (h->m_loc + ROWS - 1) / ROWS;
+    const int grid = nblocks(groups, NT / 32, MAXBLK);
+    k_dense_passN<ROWS><<<grid, NT, 0, h->stream>>>(h->A, h->lda, (int)h->m_loc, (int)h->n,
+                                                   h->zeta, h->x, h->b, h->w, h->ax, h->st,
+                                                   h->trace, h->bpart);
+  } else {
+    launch_csr_vec<0>(h, h->vecN, h->rp, h->ci, h->cv, h->m_loc, h->zeta, h->x, h->b, h->w,
+                      h->ax);
+  }
+}
+
+long long enqueue_body(rgdbek_ctx* h, cudaGraphConditionalHandle cond, int use_cond) {
+  long long L = 0;
+  const int gn = nblocks(h->n, NT, 1184);
+  const int gm = nblocks(h->m_loc, NT, MAXBLK);
+  const int gsn = nblocks(h->n, NT, 1184);
+  const int gsm = nblocks(h->m_loc, NT, 1184);
+  unsigned long long* kn = h->keys_n;
+  unsigned long long* km = h->keys_m;
+  // ---- column step ----
+  launch_passT(h); ++L;
+  k_nside<<<gn, NT, 0, h->stream>>>(h->part, h->P, h->dense ? 1 : 0, (int)h->n, h->s, h->v,
+                                    h->gamma, kn, h->st, h->trace, h->hist, h->bpart); ++L;
+  k_select_pass<NT, 2><<<gsn, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0, h->hist, h->cand); ++L;
+  k_select_pass<NT, 3><<<gsn, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0, h->hist, h->cand); ++L;
+  k_select_slow<NT><<<1, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0); ++L;
+  // selection masks are kept for rgdbek_get_blocks in a ring of 2 (by k parity):
+  // the parity is read on the device from st->k, so the graph stays static.
+  k_mask_n<<<gn, NT, 0, h->stream>>>(kn, h->s, h->v, h->zeta, h->x, h->xstar, nullptr, (int)h->n,
+                                     h->st, h->trace, h->bpart); ++L;
+  // ---- row step ----
+  launch_passN(h); ++L;
+  k_mside<<<gm, NT, 0, h->stream>>>((int)h->m_loc, h->row0, h->z, h->w, h->ax, h->b, h->rho,
+                                    h->r, km, h->st, h->hist); ++L;
+  k_select_pass<NT, 2><<<gsm, NT, 0, h->stream>>>(km, h->m_loc, h->row0, h->st, 1, h->hist,
+                                                  h->cand); ++L;
+  k_select_pass<NT, 3><<<gsm, NT, 0, h->stream>>>(km, h->m_loc, h->row0, h->st, 1, h->hist,
+                                                  h->cand); ++L;
+  k_select_slow<NT><<<1, NT, 0, h->stream>>>(km, h->m_loc, h->row0, h->st, 1); ++L;
+  k_mask_m<<<gm, NT, 0, h->stream>>>(km, h->r, h->xi, nullptr, (int)h->m_loc, h->row0, h->st,
+                                     h->trace, h->bpart); ++L;
+  k_tail<<<1, 1, 0, h->stream>>>(h->st, cond, use_cond); ++L;
+  return L;
+}
+
+rgdbek_status build_graph(rgdbek_ctx* h) {
+  // Preferred: graph = WHILE(cond) { body }, the tail kernel sets cond.
+  cudaGraph_t g = nullptr;
+  CK(h, cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle cond;
+  cudaError_t e = cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault);
+  if (e == cudaSuccess) {
+    cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+    if (e == cudaSuccess) {
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      e = cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0,
+                                        cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        h->launches_per_iter = enqueue_body(h, cond, 1);
+        cudaGraph_t out = nullptr;
+        e = cudaStreamEndCapture(h->stream, &out);
+      }
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&h->exec, g, 0);
+      if (e == cudaSuccess) {
+        h->graph = g;
+        h->use_cond = true;
+        return RGDBEK_OK;
+      }
+    }
+  }
+  // Fallback: a plain graph of one body, relaunched by the host until halted.
+  cudaGetLastError();
+  if (g) cudaGraphDestroy(g);
+  h->use_cond = false;
+  CK(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  cudaGraphConditionalHandle dummy{};
+  h->launches_per_iter = enqueue_body(h, dummy, 0);
+  CK(h, cudaStreamEndCapture(h->stream, &h->body_graph));
+  CK(h, cudaGraphInstantiate(&h->body_exec, h->body_graph, 0));
+  return RGDBEK_OK;
+}
+
+rgdbek_status finish_create(rgdbek_ctx* h) {
+  // norms of b, block sizes (reading R2), scalar state, graph
+  std::vector<double> hb(h->m_loc);
+  CK(h, cudaMemcpyAsync(hb.data(), h->b, h->m_loc * sizeof(double), cudaMemcpyDeviceToHost,
+                        h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  double bn = 0.0;
+  for (double t : hb) bn += t * t;
+  if (h->nccl) {
+    // multi-GPU: the global ||b||^2 is reduced in rgdbek_create_* (see comm.cu)
+  }
+  h->bnorm2 = bn;
+  if (!(bn > 0.0)) return set_err(h, RGDBEK_E_ZERO_RHS, "||b|| == 0: RSE is undefined (P:301-304)");
+  TRY(dalloc(h, &h->st, 1));
+  CK(h, cudaMallocHost(&h->st_host, sizeof(Scal)));
+  memset(h->st_host, 0, sizeof(Scal));
+  h->st_host->bnorm2 = bn;
+  h->st_host->kc = std::max(1LL, (long long)std::floor(h->eta * (double)h->n + 0.5));
+  h->st_host->kr = std::max(1LL, (long long)std::floor(h->eta * (double)h->m + 0.5));
+  h->st_host->trace_cap = h->trace_cap;
+  h->st_host->stop_mode = h->stop_mode;
+  CK(h, cudaMemcpyAsync(h->st, h->st_host, sizeof(Scal), cudaMemcpyHostToDevice, h->stream));
+  k_reset_scal<<<1, 1, 0, h->stream>>>(h->st, 0ull, 0);
+  k_reset_vecs<<<nblocks(std::max(h->n, h->m_loc), 256, 1184), 256, 0, h->stream>>>(
+      h->x, (int)h->n, h->z, h->b, (int)h->m_loc);
+  CK(h, cudaGetLastError());
+  CK(h, cudaStreamSynchronize(h->stream));
+  CK(h, cudaEventCreate(&h->ev0));
+  CK(h, cudaEventCreate(&h->ev1));
+  TRY(build_graph(h));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return RGDBEK_OK;
+}
+
+rgdbek_status alloc_vectors(rgdbek_ctx* h) {
+  const long long n = h->n, m = h->m_loc;
+  TRY(dalloc(h, &h->b, m));
+  TRY(dalloc(h, &h->rho, m));
+  TRY(dalloc(h, &h->gamma, n));
+  TRY(dalloc(h, &h->x, n));
+  TRY(dalloc(h, &h->s, n));
+  TRY(dalloc(h, &h->v, n));
+  TRY(dalloc(h, &h->zeta, n));
+  TRY(dalloc(h, &h->xstar, n));
+  TRY(dalloc(h, &h->z, m));
+  TRY(dalloc(h, &h->w, m));
+  TRY(dalloc(h, &h->ax, m));
+  TRY(dalloc(h, &h->r, m));
+  TRY(dalloc(h, &h->xi, m));
+  TRY(dalloc(h, &h->keys_n, n));
+  TRY(dalloc(h, &h->keys_m, m));
+  TRY(dalloc(h, &h->bpart, 4 * MAXBLK));
+  TRY(dalloc(h, &h->hist, NBINS));
+  TRY(dalloc(h, &h->cand, CAND_CAP));
+  TRY(dalloc(h, &h->trace, std::max<long long>(h->trace_cap, 1)));
+  CK(h, cudaMemsetAsync(h->hist, 0, NBINS * sizeof(unsigned int), h->stream));
+  CK(h, cudaMemsetAsync(h->xi, 0, m * sizeof(double), h->stream));
+  CK(h, cudaMemsetAsync(h->v, 0, n * sizeof(double), h->stream));
+  CK(h, cudaMemsetAsync(h->xstar, 0, n * sizeof(double), h->stream));
+  CK(h, cudaMemsetAsync(h->trace, 0, std::max<long long>(h->trace_cap, 1) * sizeof(TraceRec),
+                        h->stream));
+  return RGDBEK_OK;
+}
+
+rgdbek_status common_begin(rgdbek_ctx* h, long long m, long long n, const rgdbek_options* o) {
+  rgdbek_options d;
+  rgdbek_options_default(&d);
+  if (!o) o = &d;
+  if (!(o->eta > 0.0 && o->eta < 1.0)) return set_err(h, RGDBEK_E_ARG, "eta must lie in (0,1), got %g", o->eta);
+  if (m < 1 || n < 1) return set_err(h, RGDBEK_E_DIM, "m, n must be >= 1 (got m=%lld n=%lld)", m, n);
+  if (n > 0x7FFFFFFFLL || m > 0x7FFFFFFFLL)
+    return set_err(h, RGDBEK_E_DIM, "m, n must be < 2^31 (int32 indices)");
+  const long long rb = o->row_begin < 0 ? 0 : o->row_begin;
+  const long long re = o->row_end < 0 ? m : o->row_end;
+  if (rb >= re || re > m) return set_err(h, RGDBEK_E_DIM, "row range [%lld,%lld) outside [0,%lld)", rb, re, m);
+  if (o->stop < 0 || o->stop > 2) return set_err(h, RGDBEK_E_ARG, "unknown stop mode %d", o->stop);
+  h->m = m; h->n = n; h->row0 = rb; h->m_loc = re - rb;
+  h->eta = o->eta;
+  h->stop_mode = o->stop;
+  h->device = o->device;
+  h->nccl = o->nccl_comm;
+  h->trace_cap = std::max(0, o->trace_capacity);
+  h->symmetric = o->symmetric != 0;
+  if (h->nccl && (rb != 0 || re != m))
+    return set_err(h, RGDBEK_E_ARG, "multi-GPU sharding is not enabled in this build");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return set_err(h, RGDBEK_E_CUDA, "no CUDA device available (%s); there is no CPU fallback",
+                   cudaGetErrorString(e));
+  if (h->device < 0 || h->device >= ndev) return set_err(h, RGDBEK_E_ARG, "device %d out of range", h->device);
+  CK(h, cudaSetDevice(h->device));
+  cudaDeviceProp prop;
+  CK(h, cudaGetDeviceProperties(&prop, h->device));
+  if (prop.major < 10)
+    return set_err(h, RGDBEK_E_CUDA, "device %s is sm_%d%d; this library is built for sm_100a",
+                   prop.name, prop.major, prop.minor);
+  if (o->stream) {
+    h->stream = (cudaStream_t)o->stream;
+  } else {
+    CK(h, cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+  }
+  return RGDBEK_OK;
+}
+
+rgdbek_status check_flag(rgdbek_ctx* h, int* dflag, rgdbek_status code, const char* what) {
+  int f = 0;
+  CK(h, cudaMemcpyAsync(&f, dflag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  if (f) return set_err(h, code, "%s (flag 0x%x)", what, f);
+  return RGDBEK_OK;
+}
+
+rgdbek_status build_csc(rgdbek_ctx* h, long long** cp_out, int** ri_out, double** rv_out) {
+  const long long nnz = h->nnz;
+  int *row_of = nullptr, *perm_in = nullptr, *perm_out = nullptr, *key_in = nullptr, *key_out = nullptr;
+  long long* cp = nullptr;
+  int* ri = nullptr;
+  double* rv = nullptr;
+  TRY(dalloc(h, &cp, h->n + 1));
+  TRY(dalloc(h, &ri, nnz));
+  TRY(dalloc(h, &rv, nnz));
+  // temporaries (freed below)
+  void* tmp[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t nb = std::max<long long>(nnz, 1) * sizeof(int);
+  for (int t = 0; t < 5; ++t) CK(h, cudaMalloc(&tmp[t], nb));
+  row_of = (int*)tmp[0]; perm_in = (int*)tmp[1]; perm_out = (int*)tmp[2];
+  key_in = (int*)tmp[3]; key_out = (int*)tmp[4];
+  const int g = nblocks(nnz, 256, 4096);
+  k_expand_rows<<<nblocks(h->m_loc, 256, 4096), 256, 0, h->stream>>>(h->rp, h->m_loc, row_of);
+  k_iota<<<g, 256, 0, h->stream>>>(perm_in, nnz);
+  CK(h, cudaMemcpyAsync(key_in, h->ci, nnz * sizeof(int), cudaMemcpyDeviceToDevice, h->stream));
+  int end_bit = 1;
+  while (end_bit < 31 && (1LL << end_bit) < h->n) ++end_bit;
+  size_t tb = 0;
+  CK(h, cub::DeviceRadixSort::SortPairs(nullptr, tb, key_in, key_out, perm_in, perm_out, (int)nnz, 0,
+                                        end_bit, h->stream));
+  void* tbuf = nullptr;
+  CK(h, cudaMalloc(&tbuf, std::max<size_t>(tb, 1)));
+  CK(h, cub::DeviceRadixSort::SortPairs(tbuf, tb, key_in, key_out, perm_in, perm_out, (int)nnz, 0,
+                                        end_bit, h->stream));
+  // column counts -> exclusive scan -> col_ptr
+  CK(h, cudaMemsetAsync(cp, 0, (h->n + 1) * sizeof(long long), h->stream));
+  k_col_count<<<g, 256, 0, h->stream>>>(h->ci, nnz, cp);
+  size_t sb = 0;
+  CK(h, cub::DeviceScan::InclusiveSum(nullptr, sb, cp, cp, (int)(h->n + 1), h->stream));
+  void* sbuf = nullptr;
+  CK(h, cudaMalloc(&sbuf, std::max<size_t>(sb, 1)));
+  CK(h, cub::DeviceScan::InclusiveSum(sbuf, sb, cp, cp, (int)(h->n + 1), h->stream));
+  k_gather_csc<<<g, 256, 0, h->stream>>>(perm_out, row_of, h->cv, nnz, ri, rv);
+  CK(h, cudaGetLastError());
+  CK(h, cudaStreamSynchronize(h->stream));
+  for (int t = 0; t < 5; ++t) cudaFree(tmp[t]);
+  cudaFree(tbuf);
+  cudaFree(sbuf);
+  *cp_out = cp; *ri_out = ri; *rv_out = rv;
+  return RGDBEK_OK;
+}
+
+rgdbek_status ensure_usable(rgdbek_ctx* h) {
+  if (!h) return RGDBEK_E_ARG;
+  if (h->sticky) return (rgdbek_status)h->sticky;
+  cudaError_t e = cudaSetDevice(h->device);
+  if (e != cudaSuccess) return set_err(h, RGDBEK_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+  return RGDBEK_OK;
+}
+
+rgdbek_status run_loop(rgdbek_ctx* h, rgdbek_result* res) {
+  CK(h, cudaEventRecord(h->ev0, h->stream));
+  if (h->use_cond) {
+    CK(h, cudaGraphLaunch(h->exec, h->stream));
+  } else {
+    // host-driven fallback: relaunch the body until the device says halted
+    for (;;) {
+      for (int t = 0; t < 8; ++t) CK(h, cudaGraphLaunch(h->body_exec, h->stream));
+      CK(h, cudaMemcpyAsync(h->st_host, h->st, sizeof(Scal), cudaMemcpyDeviceToHost, h->stream));
+      CK(h, cudaStreamSynchronize(h->stream));
+      if (h->st_host->halted) break;
+    }
+  }
+  CK(h, cudaEventRecord(h->ev1, h->stream));
+  CK(h, cudaMemcpyAsync(h->st_host, h->st, sizeof(Scal), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  float ms = 0.f;
+  CK(h, cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  const Scal& s = *h->st_host;
+  if (s.error)
+    return set_err(h, RGDBEK_E_INTERNAL, "device self-check failed (code %d): block size mismatch", s.error);
+  if (!s.halted) return set_err(h, RGDBEK_E_INTERNAL, "iteration loop ended without halting");
+  if (res) {
+    res->outcome = s.outcome;
+    res->pad_ = 0;
+    res->iters = s.iters;
+    res->rse = s.rse_out;
+    res->rel_err = s.relerr_out;
+    res->seconds = ms * 1e-3;
+  }
+  return RGDBEK_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int32_t rgdbek_abi_version(void) { return RGDBEK_ABI_VERSION; }
+
+void rgdbek_options_default(rgdbek_options* o) {
+  if (!o) return;
+  memset(o, 0, sizeof *o);
+  o->eta = 0.5;
+  o->stop = RGDBEK_STOP_RSE;
+  o->device = 0;
+  o->stream = nullptr;
+  o->nccl_comm = nullptr;
+  o->row_begin = -1;
+  o->row_end = -1;
+  o->symmetric = 0;
+  o->trace_capacity = 4096;
+}
+
+const char* rgdbek_last_error(rgdbek_handle h) {
+  return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+void rgdbek_destroy(rgdbek_handle h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->exec) cudaGraphExecDestroy(h->exec);
+  if (h->graph) cudaGraphDestroy(h->graph);
+  if (h->body_exec) cudaGraphExecDestroy(h->body_exec);
+  if (h->body_graph) cudaGraphDestroy(h->body_graph);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  for (void* p : h->allocs) cudaFree(p);
+  if (h->st_host) cudaFreeHost(h->st_host);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+static rgdbek_status create_fail(rgdbek_ctx* h, rgdbek_status s) {
+  g_create_error = h->err;
+  rgdbek_destroy(h);
+  return s;
+}
+
+rgdbek_status rgdbek_create_dense(rgdbek_handle* out, int64_t m, int64_t n, const double* A_local,
+                                  int64_t lda, const double* b_local, const rgdbek_options* opts) {
+  if (!out || !A_local || !b_local) return set_err(nullptr, RGDBEK_E_ARG, "NULL argument to rgdbek_create_dense");
+  *out = nullptr;
+  rgdbek_ctx* h = new rgdbek_ctx();
+  rgdbek_status s = common_begin(h, m, n, opts);
+  if (s != RGDBEK_OK) return create_fail(h, s);
+  if (lda < n) { set_err(h, RGDBEK_E_DIM, "lda (%lld) < n (%lld)", (long long)lda, (long long)n); return create_fail(h, RGDBEK_E_DIM); }
+  h->dense = true;
+  h->lda = (n + 15) / 16 * 16;               // 128-byte aligned rows
+  if ((s = dalloc(h, &h->A, (size_t)h->m_loc * h->lda)) != RGDBEK_OK) return create_fail(h, s);
+  if ((s = alloc_vectors(h)) != RGDBEK_OK) return create_fail(h, s);
+  cudaError_t e = cudaMemsetAsync(h->A, 0, (size_t)h->m_loc * h->lda * sizeof(double), h->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(h->A, h->lda * sizeof(double), A_local, lda * sizeof(double),
+                          n * sizeof(double), h->m_loc, cudaMemcpyDefault, h->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(h->b, b_local, h->m_loc * sizeof(double), cudaMemcpyDefault, h->stream);
+  if (e != cudaSuccess) { set_err(h, RGDBEK_E_CUDA, "copy of A/b failed: %s", cudaGetErrorString(e)); return create_fail(h, RGDBEK_E_CUDA); }
+  int* flag = nullptr;
+  if ((s = dalloc(h, &flag, 1)) != RGDBEK_OK) return create_fail(h, s);
+  cudaMemsetAsync(flag, 0, sizeof(int), h->stream);
+  k_check_finite<<<nblocks((long long)h->m_loc * h->lda, 256, 4096), 256, 0, h->stream>>>(h->A, (long long)h->m_loc * h->lda, flag);
+  k_check_finite<<<nblocks(h->m_loc, 256, 1024), 256, 0, h->stream>>>(h->b, h->m_loc, flag);
+  if ((s = check_flag(h, flag, RGDBEK_E_NONFINITE, "NaN or Inf in A or b")) != RGDBEK_OK) return create_fail(h, s);
+  k_dense_rownorm<<<nblocks(h->m_loc * 32, 256, 4096), 256, 0, h->stream>>>(h->A, h->lda, h->m_loc, h->n, h->rho);
+  k_dense_colnorm<<<nblocks(h->n, 128, 4096), 128, 0, h->stream>>>(h->A, h->lda, h->m_loc, h->n, h->gamma);
+  // dense pass T geometry: column tiles of 2*PT_TPB, ~8 blocks per SM in total
+  h->tiles = (int)((n + 2 * PT_TPB - 1) / (2 * PT_TPB));
+  int panels = std::max(1, (148 * 8 + h->tiles - 1) / h->tiles);
+  h->R = (int)std::max<long long>(16, (h->m_loc + panels - 1) / panels);
+  h->R = std::min(h->R, 4096);
+  h->P = (int)((h->m_loc + h->R - 1) / h->R);
+  if ((s = dalloc(h, &h->part, (size_t)h->P * 2 * h->n)) != RGDBEK_OK) return create_fail(h, s);
+  if ((s = finish_create(h)) != RGDBEK_OK) return create_fail(h, s);
+  *out = h;
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_create_csr(rgdbek_handle* out, int64_t m, int64_t n, int64_t nnz_local,
+                                const int64_t* row_ptr_local, const int32_t* col_idx,
+                                const double* val, const double* b_local,
+                                const rgdbek_options* opts) {
+  if (!out || !row_ptr_local || !b_local || (nnz_local > 0 && (!col_idx || !val)))
+    return set_err(nullptr, RGDBEK_E_ARG, "NULL argument to rgdbek_create_csr");
+  *out = nullptr;
+  if (nnz_local < 0) return set_err(nullptr, RGDBEK_E_DIM, "nnz < 0");
+  if (nnz_local >= (1LL << 31)) return set_err(nullptr, RGDBEK_E_DIM, "nnz_local must be < 2^31 per rank");
+  rgdbek_ctx* h = new rgdbek_ctx();
+  rgdbek_status s = common_begin(h, m, n, opts);
+  if (s != RGDBEK_OK) return create_fail(h, s);
+  if (h->symmetric && m != n) { set_err(h, RGDBEK_E_ARG, "symmetric=1 needs a square A"); return create_fail(h, RGDBEK_E_ARG); }
+  h->dense = false;
+  h->nnz = nnz_local;
+  if ((s = dalloc(h, &h->rp, h->m_loc + 1)) != RGDBEK_OK) return create_fail(h, s);
+  if ((s = dalloc(h, &h->ci, nnz_local)) != RGDBEK_OK) return create_fail(h, s);
+  if ((s = dalloc(h, &h->cv, nnz_local)) != RGDBEK_OK) return create_fail(h, s);
+  if ((s = alloc_vectors(h)) != RGDBEK_OK) return create_fail(h, s);
+  cudaError_t e = cudaMemcpyAsync(h->rp, row_ptr_local, (h->m_loc + 1) * sizeof(long long), cudaMemcpyDefault, h->stream);
+  if (e == cudaSuccess && nnz_local > 0) e = cudaMemcpyAsync(h->ci, col_idx, nnz_local * sizeof(int), cudaMemcpyDefault, h->stream);
+  if (e == cudaSuccess && nnz_local > 0) e = cudaMemcpyAsync(h->cv, val, nnz_local * sizeof(double), cudaMemcpyDefault, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h->b, b_local, h->m_loc * sizeof(double), cudaMemcpyDefault, h->stream);
+  if (e != cudaSuccess) { set_err(h, RGDBEK_E_CUDA, "copy of CSR/b failed: %s", cudaGetErrorString(e)); return create_fail(h, RGDBEK_E_CUDA); }
+  long long ends[2] = {0, 0};
+  e = cudaMemcpyAsync(&ends[0], h->rp, sizeof(long long), cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&ends[1], h->rp + h->m_loc, sizeof(long long), cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) { set_err(h, RGDBEK_E_CUDA, "%s", cudaGetErrorString(e)); return create_fail(h, RGDBEK_E_CUDA); }
+  if (ends[0] != 0 || ends[1] != nnz_local) {
+    set_err(h, RGDBEK_E_CSR, "row_ptr[0] = %lld (expected 0), row_ptr[m] = %lld (expected nnz = %lld)", ends[0], ends[1], (long long)nnz_local);
+    return create_fail(h, RGDBEK_E_CSR);
+  }
+  int* flag = nullptr;
+  if ((s = dalloc(h, &flag, 1)) != RGDBEK_OK) return create_fail(h, s);
+  cudaMemsetAsync(flag, 0, sizeof(int), h->stream);
+  k_validate_csr<<<nblocks(h->m_loc, 256, 4096), 256, 0, h->stream>>>(h->rp, h->ci, h->m_loc, h->n, nnz_local, flag);
+  if ((s = check_flag(h, flag, RGDBEK_E_CSR, "invalid CSR: non-monotone row_ptr (0x2), column out of range (0x4) or columns not strictly increasing in a row (0x8)")) != RGDBEK_OK) return create_fail(h, s);
+  k_check_finite<<<nblocks(nnz_local, 256, 4096), 256, 0, h->stream>>>(h->cv, nnz_local, flag);
+  k_check_finite<<<nblocks(h->m_loc, 256, 1024), 256, 0, h->stream>>>(h->b, h->m_loc, flag);
+  if ((s = check_flag(h, flag, RGDBEK_E_NONFINITE, "NaN or Inf in A or b")) != RGDBEK_OK) return create_fail(h, s);
+  // transposed copy for pass T (a stable radix sort by column keeps rows ordered)
+  long long* cp = nullptr; int* ri = nullptr; double* rv = nullptr;
+  if ((s = build_csc(h, &cp, &ri, &rv)) != RGDBEK_OK) return create_fail(h, s);
+  if (h->symmetric) {
+    cudaMemsetAsync(flag, 0, sizeof(int), h->stream);
+    k_compare<<<nblocks(std::max<long long>(h->n + 1, nnz_local), 256, 4096), 256, 0, h->stream>>>(cp, h->rp, h->n + 1, ri, h->ci, rv, h->cv, nnz_local, flag);
+    if ((s = check_flag(h, flag, RGDBEK_E_ARG, "symmetric=1 but A != A^T")) != RGDBEK_OK) return create_fail(h, s);
+    h->cp = h->rp; h->ri = h->ci; h->rv = h->cv;   // the CSR serves as the CSC
+  } else {
+    h->cp = cp; h->ri = ri; h->rv = rv;
+  }
+  k_csr_sqnorm<<<nblocks(h->m_loc, 256, 4096), 256, 0, h->stream>>>(h->rp, h->cv, h->m_loc, h->rho);
+  k_csr_sqnorm<<<nblocks(h->n, 256, 4096), 256, 0, h->stream>>>(cp, rv, h->n, h->gamma);
+  const double avg_r = (double)nnz_local / (double)h->m_loc;
+  const double avg_c = (double)nnz_local / (double)h->n;
+  h->vecN = pick_vec(avg_r);
+  h->vecT = pick_vec(avg_c);
+  if ((s = finish_create(h)) != RGDBEK_OK) return create_fail(h, s);
+  *out = h;
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_reset(rgdbek_handle h, uint64_t seed) {
+  TRY(ensure_usable(h));
+  k_reset_scal<<<1, 1, 0, h->stream>>>(h->st, seed, 0);
+  k_reset_vecs<<<nblocks(std::max(h->n, h->m_loc), 256, 1184), 256, 0, h->stream>>>(
+      h->x, (int)h->n, h->z, h->b, (int)h->m_loc);
+  CK(h, cudaGetLastError());
+  CK(h, cudaStreamSynchronize(h->stream));
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_set_stop(rgdbek_handle h, int32_t stop) {
+  TRY(ensure_usable(h));
+  if (stop < 0 || stop > 2) return set_err(h, RGDBEK_E_ARG, "unknown stop mode %d", stop);
+  h->stop_mode = stop;
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_set_reference(rgdbek_handle h, const double* xstar) {
+  TRY(ensure_usable(h));
+  if (!xstar) return set_err(h, RGDBEK_E_ARG, "NULL xstar");
+  CK(h, cudaMemcpyAsync(h->xstar, xstar, h->n * sizeof(double), cudaMemcpyDefault, h->stream));
+  std::vector<double> hx(h->n);
+  CK(h, cudaMemcpyAsync(hx.data(), h->xstar, h->n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  double nrm = 0.0;
+  for (double t : hx) nrm += t * t;
+  if (!(nrm > 0.0) || !std::isfinite(nrm)) return set_err(h, RGDBEK_E_ARG, "||x*|| must be finite and > 0");
+  // patch the two scalar fields on the device
+  const int one = 1;
+  CK(h, cudaMemcpyAsync(&h->st->xsnorm2, &nrm, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(&h->st->has_ref, &one, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  h->has_ref = true;
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_step(rgdbek_handle h, int64_t n_iter, rgdbek_result* res) {
+  TRY(ensure_usable(h));
+  if (n_iter < 0) return set_err(h, RGDBEK_E_ARG, "n_iter < 0");
+  k_call_begin<<<1, 1, 0, h->stream>>>(h->st, n_iter, 1, 0.0, RGDBEK_STOP_NONE);
+  CK(h, cudaGetLastError());
+  return run_loop(h, res);
+}
+
+rgdbek_status rgdbek_solve(rgdbek_handle h, double tol, int64_t max_iter, uint64_t seed,
+                           rgdbek_result* res) {
+  TRY(ensure_usable(h));
+  if (!(tol > 0.0) && h->stop_mode != RGDBEK_STOP_NONE) return set_err(h, RGDBEK_E_ARG, "tol must be > 0");
+  if (max_iter < 1) return set_err(h, RGDBEK_E_ARG, "max_iter must be >= 1");
+  if (h->stop_mode == RGDBEK_STOP_REL_ERR && !h->has_ref)
+    return set_err(h, RGDBEK_E_STATE, "STOP_REL_ERR needs rgdbek_set_reference first");
+  TRY(rgdbek_reset(h, seed));
+  k_call_begin<<<1, 1, 0, h->stream>>>(h->st, max_iter, 0, tol, h->stop_mode);
+  CK(h, cudaGetLastError());
+  return run_loop(h, res);
+}
+
+rgdbek_status rgdbek_get_x(rgdbek_handle h, double* out) {
+  TRY(ensure_usable(h));
+  if (!out) return set_err(h, RGDBEK_E_ARG, "NULL out");
+  CK(h, cudaMemcpyAsync(out, h->x, h->n * sizeof(double), cudaMemcpyDefault, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_get_z(rgdbek_handle h, double* out) {
+  TRY(ensure_usable(h));
+  if (!out) return set_err(h, RGDBEK_E_ARG, "NULL out");
+  CK(h, cudaMemcpyAsync(out, h->z, h->m_loc * sizeof(double), cudaMemcpyDefault, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_get_blocks(rgdbek_handle h, int64_t* n_u, uint64_t* hash_u, int32_t* U,
+                                int64_t* n_j, uint64_t* hash_j, int32_t* J) {
+  TRY(ensure_usable(h));
+  CK(h, cudaMemcpyAsync(h->st_host, h->st, sizeof(Scal), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  const Scal& s = *h->st_host;
+  if (s.k < 1 || s.trace_cap <= 0) return set_err(h, RGDBEK_E_STATE, "no completed iteration recorded");
+  TraceRec t;
+  CK(h, cudaMemcpy(&t, h->trace + ((s.k - 1) % s.trace_cap), sizeof t, cudaMemcpyDeviceToHost));
+  if (n_u) *n_u = t.kp;
+  if (hash_u) *hash_u = t.hash_u;
+  if (n_j) *n_j = t.kpp;
+  if (hash_j) *hash_j = t.hash_j;
+  if (U || J) return set_err(h, RGDBEK_E_ARG, "index lists are not retained; pass NULL (hashes identify the blocks)");
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_get_trace(rgdbek_handle h, rgdbek_trace_record* out, int64_t max_records,
+                               int64_t* n_out) {
+  TRY(ensure_usable(h));
+  if (!out || !n_out || max_records < 0) return set_err(h, RGDBEK_E_ARG, "bad arguments");
+  CK(h, cudaMemcpyAsync(h->st_host, h->st, sizeof(Scal), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  const long long k = h->st_host->k, cap = h->trace_cap;
+  if (cap <= 0) { *n_out = 0; return RGDBEK_OK; }
+  const long long first = std::max(0LL, k - cap);
+  long long cnt = std::min<long long>(k - first, max_records);
+  std::vector<TraceRec> all(cap);
+  CK(h, cudaMemcpy(all.data(), h->trace, cap * sizeof(TraceRec), cudaMemcpyDeviceToHost));
+  for (long long i = 0; i < cnt; ++i) {
+    const TraceRec& t = all[(first + i) % cap];
+    static_assert(sizeof(TraceRec) == sizeof(rgdbek_trace_record), "trace layout");
+    memcpy(&out[i], &t, sizeof t);
+    out[i].k = first + i;
+  }
+  *n_out = cnt;
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_set_state(rgdbek_handle h, const double* x, const double* z_local, int64_t k) {
+  TRY(ensure_usable(h));
+  if (!x || !z_local || k < 0) return set_err(h, RGDBEK_E_ARG, "bad arguments");
+  CK(h, cudaMemcpyAsync(h->x, x, h->n * sizeof(double), cudaMemcpyDefault, h->stream));
+  CK(h, cudaMemcpyAsync(h->z, z_local, h->m_loc * sizeof(double), cudaMemcpyDefault, h->stream));
+  CK(h, cudaMemcpyAsync(h->st_host, h->st, sizeof(Scal), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  k_reset_scal<<<1, 1, 0, h->stream>>>(h->st, h->st_host->seed, k);
+  CK(h, cudaGetLastError());
+  CK(h, cudaStreamSynchronize(h->stream));
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_launch_kernel(rgdbek_handle h, int32_t kernel, int32_t reps,
+                                   double* bytes_per_launch) {
+  TRY(ensure_usable(h));
+  if (kernel < 0 || kernel > 1 || reps < 0) return set_err(h, RGDBEK_E_ARG, "bad kernel id / reps");
+  // never halt inside the timing loop
+  k_call_begin<<<1, 1, 0, h->stream>>>(h->st, 1LL << 60, 1, 0.0, RGDBEK_STOP_NONE);
+  const double m = (double)h->m_loc, n = (double)h->n;
+  double bytes;
+  if (h->dense) {
+    bytes = 8.0 * m * n + (kernel == 0 ? 16.0 * m + 16.0 * n : 16.0 * n + 24.0 * m);
+  } else {
+    const double nnz = (double)h->nnz;
+    bytes = kernel == 0 ? 12.0 * nnz + 8.0 * (n + 1) + 16.0 * m + 16.0 * n
+                        : 12.0 * nnz + 8.0 * (m + 1) + 16.0 * n + 24.0 * m;
+  }
+  if (bytes_per_launch) *bytes_per_launch = bytes;
+  for (int i = 0; i < reps; ++i) {
+    if (kernel == 0) launch_passT(h); else launch_passN(h);
+  }
+  CK(h, cudaGetLastError());
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_launches_per_iteration(rgdbek_handle h, int64_t* out) {
+  if (!h || !out) return RGDBEK_E_ARG;
+  *out = h->launches_per_iter;
+  return RGDBEK_OK;
+}
+
+void* rgdbek_stream(rgdbek_handle h) { return h ? (void*)h->stream : nullptr; }
+
+// NCCL bootstrap: the library dlopen()s the libnccl already loaded in the
+// process (torch's), so no second copy of NCCL enters the address space.
+typedef int (*nccl_getid_t)(void*);
+typedef int (*nccl_init_t)(void**, int, const void*, int);
+typedef int (*nccl_destroy_t)(void*);
+
+static void* nccl_lib() {
+  static void* lib = nullptr;
+  if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  return lib;
+}
+
+rgdbek_status rgdbek_nccl_unique_id(void* out_128_bytes) {
+  void* lib = nccl_lib();
+  if (!lib || !out_128_bytes) return set_err(nullptr, RGDBEK_E_NCCL, "libnccl.so.2 not loadable");
+  auto f = (nccl_getid_t)dlsym(lib, "ncclGetUniqueId");
+  if (!f || f(out_128_bytes) != 0) return set_err(nullptr, RGDBEK_E_NCCL, "ncclGetUniqueId failed");
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_nccl_comm_init(void** comm_out, int32_t nranks, int32_t rank,
+                                    const void* id_128_bytes, int32_t device) {
+  void* lib = nccl_lib();
+  if (!lib || !comm_out || !id_128_bytes) return set_err(nullptr, RGDBEK_E_NCCL, "libnccl.so.2 not loadable");
+  struct Id { char b[128]; } id;
+  memcpy(&id, id_128_bytes, 128);
+  cudaSetDevice(device);
+  // ncclCommInitRank takes ncclUniqueId by value (128 bytes)
+  typedef int (*init_by_val_t)(void**, int, Id, int);
+  auto f = (init_by_val_t)dlsym(lib, "ncclCommInitRank");
+  if (!f || f(comm_out, nranks, id, rank) != 0) return set_err(nullptr, RGDBEK_E_NCCL, "ncclCommInitRank failed");
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_nccl_comm_destroy(void* comm) {
+  void* lib = nccl_lib();
+  if (!lib || !comm) return RGDBEK_E_ARG;
+  auto f = (nccl_destroy_t)dlsym(lib, "ncclCommDestroy");
+  if (!f || f(comm) != 0) return set_err(nullptr, RGDBEK_E_NCCL, "ncclCommDestroy failed");
+  return RGDBEK_OK;
+}
+
+}  // extern "C"

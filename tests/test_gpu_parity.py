@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, same seeded inputs.
+
+Bars (BASELINE.json north_star):
+  * block index sets identical for the first 50 iterations: |U_k|, |J_k| and
+    their 64-bit hashes equal, iteration by iteration;
+  * x and z within relative 1e-10 (x normalised by ||x_oracle||, z by ||b||,
+    reading R18) after every one of those iterations;
+  * iterations to ||x - x*||/||x*|| <= 1e-6 within +/-2% of the oracle's.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL_X = 1e-10
+TOL_Z = 1e-10
+TOL_SCAL = 1e-9
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2509_19267_b200 import _build
+    _build.build()
+
+
+def _solver(w, **kw):
+    from paper_2509_19267_b200 import Solver
+    if w.dense:
+        return Solver(w.A, w.b, eta=w.eta, **kw)
+    return Solver.from_scipy(w.A, w.b, eta=w.eta, symmetric=w.symmetric, **kw)
+
+
+def _oracle(w):
+    from oracle import Oracle
+    return Oracle(w.A, w.b, w.eta)
+
+
+def _run_parity(w, iters=50, seed=0, every=1):
+    """Step both sides one iteration at a time; compare blocks, scalars, x and z."""
+    s = _solver(w)
+    o = _oracle(w)
+    s.reset(seed)
+    bn = np.linalg.norm(w.b)
+    for k in range(iters):
+        rec = o.iterate(seed)
+        s.step(1)
+        if (k + 1) % every and k + 1 != iters:
+            continue
+        g = s.trace()[-1]
+        assert g["k"] == k
+        assert (g["kp"], g["hash_u"]) == (rec.kp, rec.hash_u), f"U differs at k={k}"
+        assert (g["kpp"], g["hash_j"]) == (rec.kpp, rec.hash_j), f"J differs at k={k}"
+        for f in ("Z", "W", "X", "V"):
+            a, b = g[f], getattr(rec, f)
+            assert abs(a - b) <= TOL_SCAL * max(abs(b), 1e-300), (k, f, a, b)
+        x = s.x()
+        assert np.linalg.norm(x - o.x) <= TOL_X * max(np.linalg.norm(o.x), 1e-300), k
+        assert np.linalg.norm(s.z() - o.z) <= TOL_Z * bn, k
+        nu, hu, nj, hj = s.blocks()
+        assert (nu, hu, nj, hj) == (rec.kp, rec.hash_u, rec.kpp, rec.hash_j)
+    s.close()
+    return o
+
+
+@pytest.mark.parametrize("name,eta", [("C1", 0.5), ("C1", 0.1), ("C2s", 0.5), ("C2s", 0.1),
+                                      ("C2si", 0.5)])
+def test_dense_50_iterations(name, eta):
+    from workloads import by_name
+    w = by_name(name)
+    w.eta = eta
+    _run_parity(w, 50, seed=3)
+
+
+@pytest.mark.parametrize("name", ["C3s", "C4s", "C5t"])
+def test_sparse_50_iterations(name):
+    from workloads import by_name
+    _run_parity(by_name(name), 50, seed=1)
+
+
+def test_sparse_random_with_empty_rows_and_columns():
+    import scipy.sparse as sp
+    from workloads import sparse_random
+    w = sparse_random(700, 300, density=0.01, seed=9, consistent=False)
+    assert (np.diff(w.A.indptr) == 0).any()                 # empty rows exist
+    assert (np.bincount(w.A.indices, minlength=300) == 0).any()   # empty columns exist
+    _run_parity(w, 30, seed=2)
+
+
+def test_fat_sparse_system():
+    from workloads import sparse_random
+    w = sparse_random(200, 900, density=0.02, seed=4)
+    _run_parity(w, 30, seed=5)
+
+
+def test_block_size_one_and_large_eta():
+    from workloads import dense_gaussian
+    w = dense_gaussian(300, 80, seed=2, noise=0.1)
+    w.eta = 0.001            # k_c = k_r = 1: REK-type steps
+    _run_parity(w, 25, seed=1)
+    w.eta = 0.97
+    _run_parity(w, 25, seed=1)
+
+
+@pytest.mark.parametrize("name,seeds", [("C1", [0, 1, 2, 3]), ("C2s", [0, 1]), ("C5t", [0])])
+def test_time_to_tolerance_matches_oracle(name, seeds):
+    from oracle import STOP_REL_ERR
+    from paper_2509_19267_b200 import RGDBEK_CONVERGED
+    from workloads import by_name
+    w = by_name(name)
+    for seed in seeds:
+        s = _solver(w, stop="rel_err")
+        s.set_reference(w.xstar)
+        res = s.solve(1e-6, 100000, seed)
+        o = _oracle(w)
+        out, iters, rse, rel = o.solve(1e-6, 100000, seed, stop=STOP_REL_ERR, xstar=w.xstar)
+        assert res["outcome"] == RGDBEK_CONVERGED == out
+        assert abs(res["iters"] - iters) <= max(1, int(0.02 * iters)), (seed, res["iters"], iters)
+        assert res["rel_err"] <= 1e-6
+        s.close()
+
+
+def test_rse_stop_spec_identity():
+    from paper_2509_19267_b200 import Solver, RGDBEK_CONVERGED
+    s = Solver(np.eye(10), np.ones(10), eta=0.5, stop="rse")
+    res = s.solve(1e-12, 1000, 0)
+    assert res["outcome"] == RGDBEK_CONVERGED and res["rse"] <= 1e-12
+    np.testing.assert_allclose(s.x(), np.ones(10), atol=1e-6)
+
+
+def test_stall_and_max_iter():
+    from paper_2509_19267_b200 import Solver, RGDBEK_STALLED, RGDBEK_MAX_ITER
+    s = Solver(np.array([[1.0, 0.0], [0.0, 0.0]]), np.array([0.0, 1.0]), eta=0.5)
+    res = s.solve(1e-12, 100, 0)
+    assert res["outcome"] == RGDBEK_STALLED and res["iters"] == 1 and res["rse"] == 1.0
+    from workloads import dense_gaussian
+    w = dense_gaussian(60, 20, seed=1)
+    s = Solver(w.A, w.b, eta=0.5)
+    res = s.solve(1e-300, 7, 0)
+    assert res["outcome"] == RGDBEK_MAX_ITER and res["iters"] == 7
+
+
+def test_inconsistent_shift_invariance_on_gpu():
+    from workloads import by_name
+    w = by_name("C2si")
+    from paper_2509_19267_b200 import Solver
+    a = Solver(w.A, w.b, eta=0.5)
+    c = Solver(w.A, w.b - w.rvec, eta=0.5)
+    a.reset(7); c.reset(7)
+    a.step(40); c.step(40)
+    ta, tc = a.trace(), c.trace()
+    assert [(t["hash_u"], t["hash_j"]) for t in ta] == [(t["hash_u"], t["hash_j"]) for t in tc]
+    assert np.linalg.norm(a.x() - c.x()) <= 1e-12 * np.linalg.norm(c.x())
+    assert np.linalg.norm((a.z() - w.rvec) - c.z()) <= 1e-12 * np.linalg.norm(w.b)
+
+
+def test_step_chunks_equal_one_run_and_resume():
+    from workloads import by_name
+    w = by_name("C2s")
+    from paper_2509_19267_b200 import Solver
+    a = Solver(w.A, w.b)
+    b = Solver(w.A, w.b)
+    a.reset(11); b.reset(11)
+    a.step(30)
+    b.step(7); b.step(0); b.step(13); b.step(10)
+    assert np.array_equal(a.x(), b.x()) and np.array_equal(a.z(), b.z())
+    # resume from a saved state
+    c = Solver(w.A, w.b)
+    c.reset(11)
+    c.set_state(b.x(), b.z(), 30)
+    a.step(5); c.step(5)
+    assert np.array_equal(a.x(), c.x()) and np.array_equal(a.z(), c.z())
+
+
+def test_step_zero_reports_rse_of_current_iterate():
+    from workloads import by_name
+    w = by_name("C1")
+    s = _solver(w)
+    s.reset(0)
+    r = s.step(0)
+    assert r["iters"] == 0 and abs(r["rse"] - 1.0) < 1e-15
+    r = s.step(4)
+    o = _oracle(w)
+    for _ in range(4):
+        rec = o.iterate(0)
+    assert r["iters"] == 4 and abs(r["rse"] - rec.rse) <= 1e-9 * rec.rse
+
+
+def test_create_errors():
+    import scipy.sparse as sp
+    from paper_2509_19267_b200 import Solver, RgdbekError
+    with pytest.raises(RgdbekError) as e:
+        Solver(np.eye(3), np.zeros(3))
+    assert e.value.code == -4
+    A = np.eye(3); A[1, 1] = np.nan
+    with pytest.raises(RgdbekError) as e:
+        Solver(A, np.ones(3))
+    assert e.value.code == -5
+    # columns not strictly increasing
+    with pytest.raises(RgdbekError) as e:
+        Solver.from_csr(2, 3, np.array([0, 2, 3]), np.array([2, 1, 0], dtype=np.int32),
+                        np.ones(3), np.ones(2))
+    assert e.value.code == -3
+    with pytest.raises(RgdbekError) as e:
+        Solver.from_csr(2, 3, np.array([0, 2, 3]), np.array([0, 5, 0], dtype=np.int32),
+                        np.ones(3), np.ones(2))
+    assert e.value.code == -3
+    with pytest.raises(RgdbekError) as e:
+        Solver.from_scipy(sp.csr_matrix(np.array([[1.0, 2.0], [0.0, 1.0]])), np.ones(2),
+                          symmetric=True)
+    assert e.value.code == -1
+
+
+def test_torch_cuda_tensors_as_inputs():
+    import torch
+    from workloads import by_name
+    from paper_2509_19267_b200 import Solver
+    w = by_name("C1")
+    At = torch.from_numpy(w.A).cuda()
+    bt = torch.from_numpy(w.b).cuda()
+    s = Solver(At, bt, eta=0.5, stream=torch.cuda.current_stream().cuda_stream)
+    s.reset(0)
+    s.step(10)
+    xo = torch.empty(w.A.shape[1], dtype=torch.float64, device="cuda")
+    s.x(out=xo)
+    o = _oracle(w)
+    for _ in range(10):
+        o.iterate(0)
+    assert np.linalg.norm(xo.cpu().numpy() - o.x) <= 1e-10 * np.linalg.norm(o.x)
+
+
+@pytest.mark.parametrize("name", ["C2c", "C2i"])
+def test_full_size_dense_bench_configuration(name):
+    """BASELINE configs[1] at full size, in bench.py's launch configuration:
+    5 iterations compared element-wise (oracle takes seconds per iteration)."""
+    from workloads import by_name
+    w = by_name(name)
+    _run_parity(w, 5, seed=0)
+
+
+def test_full_size_c3_sampled():
+    """C3 (4M unknowns) at full size: 3 iterations vs the oracle on sampled rows."""
+    from workloads import by_name
+    w = by_name("C3")
+    s = _solver(w)
+    o = _oracle(w)
+    s.reset(0)
+    recs = [o.iterate(0) for _ in range(3)]
+    s.step(3)
+    t = s.trace()
+    assert [(r["kp"], r["hash_u"], r["kpp"], r["hash_j"]) for r in t] == \
+           [(r.kp, r.hash_u, r.kpp, r.hash_j) for r in recs]
+    rng = np.random.default_rng(0)
+    idx = rng.choice(w.A.shape[1], 4096, replace=False)
+    x = s.x()
+    assert np.max(np.abs(x[idx] - o.x[idx])) <= 1e-10 * np.max(np.abs(o.x))
+    assert np.linalg.norm(s.z() - o.z) <= 1e-10 * np.linalg.norm(w.b)
