@@ -81,8 +81,16 @@ def test_sparse_random_with_empty_rows_and_columns():
     import scipy.sparse as sp
     from workloads import sparse_random
     w = sparse_random(700, 300, density=0.01, seed=9, consistent=False)
-    assert (np.diff(w.A.indptr) == 0).any()                 # empty rows exist
-    assert (np.bincount(w.A.indices, minlength=300) == 0).any()   # empty columns exist
+    A = w.A.tolil()
+    A[:, 7] = 0.0
+    A[:, 150] = 0.0
+    A[3, :] = 0.0
+    A = A.tocsr()
+    A.eliminate_zeros()
+    A.sort_indices()
+    w.A = A
+    assert (np.diff(A.indptr) == 0).any()                            # empty rows
+    assert (np.bincount(A.indices, minlength=300) == 0).any()        # empty columns
     _run_parity(w, 30, seed=2)
 
 
