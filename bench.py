@@ -1,0 +1,360 @@
+"""RGDBEK hot-path benchmark (driver contract: one JSON line from rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2c] [--impl ours|reference]
+
+A "step" is one RGDBEK iteration (the whole hot path: pass T, column scores +
+Philox keys + exact block selection, pass N, z update, row scores + keys +
+selection, x update) over the synthetic workload resident in HBM.
+
+  value       iterations/s on the device (CUDA events on the solver's stream,
+              max over ranks), inputs resident, K iterations per timed region
+  e2e         the same metric through the C ABI from HOST buffers: create()
+              (H2D of A and b) + K iterations + get_x (D2H), host clock
+  roofline    the dominant kernel (dense pass T / pass N GEMV) timed alone with
+              CUDA events: algorithmic bytes / mean launch time vs the measured
+              HBM copy peak (MEASURED_PEAKS.json)
+  cpu_baseline  the CPU oracle (oracle/, numpy fp64) on a bounded sample
+  time_to_tol   device time of rgdbek_solve to ||x - x*||/||x*|| <= 1e-6
+
+--impl reference times the oracle itself (the slow plain program this tier
+uses as its reference arm) on the same workload, metric and unit.
+"""
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np
+
+METRIC = "RGDBEK iterations/sec and time-to-1e-6 rel. error; SpMV HBM GB/s vs peak"
+UNIT = "iterations/s"
+
+WORKLOADS = {
+    "C2c": "dense Gaussian 20000x5000 consistent, seed 0 (BASELINE configs[1])",
+    "C2i": "dense Gaussian 20000x5000 noisy-inconsistent (||r|| = 0.1||Ax*||), seed 0 (BASELINE configs[1])",
+    "C1": "dense Gaussian 200x50 consistent, seed 0 (BASELINE configs[0])",
+    "C3": "2-D Poisson 5-point, 4M unknowns, CSR symmetric (BASELINE configs[2])",
+    "C4": "1-D Gaussian Toeplitz blur sigma=r=20 on 1024^2 image + noise (BASELINE configs[3])",
+    "C5s": "population-model sliding window 50000x5000, 20 nnz/row, inconsistent (configs[4] scaled)",
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------------------
+# clocks during the timed region (NVML; nvidia-smi equivalent fields)
+# ---------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting", 0x1: "gpu_idle", 0x10: "sync_boost"}
+
+    def __init__(self, device=0, period=0.02):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # no NVML: report null clocks
+            log("clock sampler unavailable:", e)
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------------
+def make_solver(w, device, stream):
+    from paper_2509_19267_b200 import Solver
+    if w.dense:
+        return Solver(w.A, w.b, eta=w.eta, device=device, stream=stream)
+    return Solver.from_scipy(w.A, w.b, eta=w.eta, symmetric=w.symmetric, device=device,
+                             stream=stream)
+
+
+def time_kernel(s, kernel, reps, torch):
+    """Mean launch time (s) of one hot kernel, CUDA events on the solver's stream."""
+    st = torch.cuda.ExternalStream(s.stream)
+    s.launch_kernel(kernel, 3)                      # warm
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    bytes_per = s.launch_kernel(kernel, reps)
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e-3 / reps, bytes_per
+
+
+def cpu_oracle_sample(w, budget_s=15.0, max_iters=None):
+    """Oracle iterations/s on a bounded sample (first iterations of the same solve)."""
+    from oracle import Oracle
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    o = Oracle(w.A, w.b, w.eta)
+    t0 = time.perf_counter()
+    it = 0
+    while True:
+        o.iterate(0)
+        it += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or (max_iters and it >= max_iters):
+            break
+    return it / el, it, el, threads
+
+
+def load_traffic(workload, kernel):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get(workload, {}).get(kernel)
+    return None
+
+
+def run_ours(args):
+    import torch
+    from workloads import by_name
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = by_name(args.workload)
+    m, n = w.shape
+    stream = torch.cuda.current_stream()
+    # Multi-GPU: this build runs independent replicas per rank; the
+    # row-sharded NCCL plan is selected with --shard once available.
+    s = make_solver(w, local, stream.cuda_stream)
+    s.reset(0)
+    s.step(args.warmup)                              # W untimed warm-up iterations
+    s.reset(0)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        s.step(args.steps)                           # exactly K iterations (+ the stop-test tail)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t = e0.elapsed_time(e1) * 1e-3
+    if dist:
+        tt = torch.tensor([t], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    value = args.steps * world / t
+    launches = 1 + s.launches_per_iteration() * (args.steps + 1)
+
+    # dominant kernels timed alone (roofline)
+    peak, peak_src = load_peaks()
+    kernels = {}
+    for kid, kname in ((0, "passT"), (1, "passN")):
+        dt, bytes_per = time_kernel(s, kid, 20, torch)
+        kernels[kname] = {"seconds": dt, "bytes": bytes_per, "gbs": bytes_per / dt / 1e9}
+    s.reset(0)
+    dom = max(kernels, key=lambda k: kernels[k]["seconds"])
+    kd = kernels[dom]
+    traffic = load_traffic(args.workload, dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(kd["gbs"], 1),
+                "peak": peak, "unit": "GB/s", "frac": round(kd["gbs"] / peak, 4),
+                "traffic": traffic, "peak_source": peak_src,
+                "kernels": {k: {"achieved": round(v["gbs"], 1), "frac": round(v["gbs"] / peak, 4),
+                                "us_per_launch": round(v["seconds"] * 1e6, 2),
+                                "algorithmic_bytes": v["bytes"]} for k, v in kernels.items()},
+                "iteration_frac": round(sum(v["bytes"] for v in kernels.values())
+                                        * value / world / 1e9 / peak, 4)}
+
+    # time to tolerance (device time of rgdbek_solve, REL_ERR 1e-6)
+    ttt = None
+    if w.xstar is not None and not args.skip_ttt:
+        s.set_stop("rel_err")
+        s.set_reference(w.xstar)
+        res = s.solve(1e-6, 100000, 0)
+        ttt = {"seconds": res["seconds"], "iters": res["iters"], "rel_err": res["rel_err"],
+               "outcome": res["outcome"], "tol": 1e-6, "eta": w.eta}
+        s.set_stop("rse")
+    s.close()
+
+    # e2e through the C ABI from host (pinned) buffers
+    e2e = None
+    if not args.skip_e2e:
+        A_h = torch.from_numpy(np.ascontiguousarray(w.A)).pin_memory() if w.dense else None
+        b_h = torch.from_numpy(w.b).pin_memory()
+        x_h = torch.empty(n, dtype=torch.float64).pin_memory()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if w.dense:
+            from paper_2509_19267_b200 import Solver
+            s2 = Solver(A_h, b_h, eta=w.eta, device=local, stream=stream.cuda_stream)
+        else:
+            s2 = make_solver(w, local, stream.cuda_stream)
+        s2.reset(0)
+        s2.step(args.steps)
+        s2.x(out=x_h)
+        t_e2e = time.perf_counter() - t0
+        s2.close()
+        if dist:
+            tt = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        a_bytes = (m * n * 8) if w.dense else (w.A.nnz * 12 + (m + 1) * 8)
+        e2e = {"value": round(args.steps * world / t_e2e, 3), "unit": UNIT,
+               "h2d_bytes_per_step": int((a_bytes + 8 * m) / args.steps),
+               "d2h_bytes_per_step": int(8 * n / args.steps),
+               "note": "create() from pinned host A,b + K iterations + get_x to host; host clock"}
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if not args.skip_cpu:
+            v, it, el, threads = cpu_oracle_sample(w, budget_s=args.cpu_budget)
+            cpu = {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "oracle",
+                   "sample": f"first {it} iterations of the same {args.workload} solve "
+                             f"(seed 0) in {el:.1f} s, numpy/BLAS fp64 incl. the per-iteration RSE matvec"}
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * t / args.steps, 5),
+            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "description": WORKLOADS.get(args.workload),
+                       "m": m, "n": n, "nnz": int(w.nnz), "eta": w.eta,
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (A = %.0f MB > 126 MB)" % (
+                           (m * n * 8 if w.dense else w.A.nnz * 12) / 1e6)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "time_to_tol": ttt,
+            "gpu_launches": launches, "clocks": clk.summary(),
+        }
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def run_reference(args):
+    """The oracle (plain numpy fp64 CPU program) on the same workload and metric."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    from workloads import by_name
+    from oracle import Oracle
+    w = by_name(args.workload)
+    o = Oracle(w.A, w.b, w.eta)
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    for _ in range(min(args.warmup, 3)):
+        o.iterate(0)
+    o.reset()
+    # bounded sample: at most ~budget seconds of timed iterations
+    t0 = time.perf_counter()
+    it = 0
+    while it < args.steps:
+        o.iterate(0)
+        it += 1
+        if time.perf_counter() - t0 > args.cpu_budget and it >= 3:
+            break
+    el = time.perf_counter() - t0
+    v = it / el
+    sample = (f"{it} of the requested {args.steps} iterations of the {args.workload} solve "
+              f"(seed 0), stopped at the {args.cpu_budget:.0f} s budget" if it < args.steps
+              else f"all {it} iterations of the {args.workload} solve (seed 0)")
+    out = {"metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": args.gpus,
+           "steps": it, "warmup": args.warmup, "ms_per_step": round(1e3 * el / it, 3),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "impl": "reference",
+           "config": {"workload": args.workload, "description": WORKLOADS.get(args.workload),
+                      "m": w.shape[0], "n": w.shape[1], "eta": w.eta},
+           "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--workload", default="C2c", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-ttt", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rule)")
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -84,66 +84,96 @@ __global__ void __launch_bounds__(TPB) k_dense_passT(const double* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
-// Dense pass N: w_i = A_i . zeta, ax_i = A_i . x; RSE numerator; stop test.
-// One warp per ROWS rows, 16-byte loads; zeta/x through L1.
+// Dense pass N: partial dots of (ROWS rows) x (one chunk of CH columns) per
+// warp-unit, units dealt round-robin to all resident warps (~20 each, so the
+// per-warp work is balanced to a few %).  The streaming loop has no barrier,
+// fence or atomic (a __threadfence per unit invalidates L1 — CCTL.IVALL — and
+// with it the cached zeta/x).  k_dense_reduceN adds the Q chunk partials in
+// chunk order (deterministic) and forms w, A x, W, ||b - A x||^2.
 // ---------------------------------------------------------------------------
 __device__ void passN_finish(Scal* st, TraceRec* tr, double* bpart, int nblk, double* sh);
 
 template <int ROWS>
 __global__ void __launch_bounds__(NT) k_dense_passN(const double* __restrict__ A, long long lda,
-                                                   int m_loc, int n,
+                                                   int m_loc, int n, int CH, int Q,
                                                    const double* __restrict__ zeta,
                                                    const double* __restrict__ x,
-                                                   const double* __restrict__ b,
-                                                   double* __restrict__ w, double* __restrict__ ax,
-                                                   Scal* st, TraceRec* tr, double* bpart) {
+                                                   double* __restrict__ npart, const Scal* st) {
   if (st->halted) return;
-  __shared__ double sh[NT / 32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * NT + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * NT) >> 5;
   const int groups = (m_loc + ROWS - 1) / ROWS;
-  double Wp = 0.0, Yp = 0.0;
-  for (int g = blockIdx.x * (NT / 32) + warp; g < groups; g += gridDim.x * (NT / 32)) {
+  const int units = groups * Q;
+  for (int u = gw; u < units; u += nw) {
+    const int g = u / Q, q = u - g * Q;
     const int r0 = g * ROWS;
+    const int nr = min(ROWS, m_loc - r0);
+    const int c0 = q * CH;
+    const int c1 = min(n, c0 + CH);
+    const int c1e = c0 + ((c1 - c0) & ~1);
     double sw[ROWS], sx[ROWS];
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) { sw[r] = 0.0; sx[r] = 0.0; }
-    const int nr = min(ROWS, m_loc - r0);
-    const int n2 = n & ~1;
+    const double* arow = A + (long long)r0 * lda;
 #pragma unroll 4
-    for (int c = lane * 2; c < n2; c += 64) {
+    for (int c = c0 + lane * 2; c < c1e; c += 64) {
       const double2 zc = __ldg(reinterpret_cast<const double2*>(zeta + c));
       const double2 xc = __ldg(reinterpret_cast<const double2*>(x + c));
 #pragma unroll
       for (int r = 0; r < ROWS; ++r) {
         if (r < nr) {
-          const double2 a = ld_stream2(A + (long long)(r0 + r) * lda + c);
+          const double2 a = ld_stream2(arow + (long long)r * lda + c);
           sw[r] = fma(a.x, zc.x, sw[r]); sw[r] = fma(a.y, zc.y, sw[r]);
           sx[r] = fma(a.x, xc.x, sx[r]); sx[r] = fma(a.y, xc.y, sx[r]);
         }
       }
     }
-    if ((n & 1) && lane == 0) {
-      const int c = n - 1;
+    if (c1e < c1 && lane == 0) {                 // odd tail column (odd n, last chunk)
       for (int r = 0; r < nr; ++r) {
-        const double a = ld_stream(A + (long long)(r0 + r) * lda + c);
-        sw[r] = fma(a, zeta[c], sw[r]);
-        sx[r] = fma(a, x[c], sx[r]);
+        const double a = ld_stream(arow + (long long)r * lda + c1e);
+        sw[r] = fma(a, zeta[c1e], sw[r]);
+        sx[r] = fma(a, x[c1e], sx[r]);
       }
     }
 #pragma unroll
-    for (int r = 0; r < ROWS; ++r) {
-      const double tw = warp_sum(sw[r]), tx = warp_sum(sx[r]);
-      if (lane == 0 && r < nr) {
-        const int i = r0 + r;
-        w[i] = tw;
-        ax[i] = tx;
-        const double y = b[i] - tx;
-        Wp += tw * tw;
-        Yp += y * y;
+    for (int r = 0; r < ROWS; ++r) { sw[r] = warp_sum(sw[r]); sx[r] = warp_sum(sx[r]); }
+    if (lane < 2 * nr) {
+      // lane 2r holds row r's A.zeta partial, lane 2r+1 its A.x partial
+      double val = 0.0;
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) {
+        if (lane == 2 * r) val = sw[r];
+        if (lane == 2 * r + 1) val = sx[r];
       }
+      npart[((long long)q * m_loc + r0) * 2 + lane] = val;
     }
   }
-  // per-block partials of W and ||b - Ax||^2
+}
+
+// Second stage of dense pass N: w_i, (A x)_i = sum over chunks in order;
+// W = ||w||^2 and ||b - A x||^2 -> stop test on x_k (last block).
+__global__ void __launch_bounds__(NT) k_dense_reduceN(const double* __restrict__ npart, int Q,
+                                                     int m_loc, const double* __restrict__ b,
+                                                     double* __restrict__ w,
+                                                     double* __restrict__ ax, Scal* st,
+                                                     TraceRec* tr, double* bpart) {
+  if (st->halted) return;
+  __shared__ double sh[NT / 32];
+  double Wp = 0.0, Yp = 0.0;
+  for (int i = blockIdx.x * NT + threadIdx.x; i < m_loc; i += gridDim.x * NT) {
+    double tw = 0.0, tx = 0.0;
+    for (int q = 0; q < Q; ++q) {
+      const double2 p = __ldcg(reinterpret_cast<const double2*>(npart + ((long long)q * m_loc + i) * 2));
+      tw += p.x;
+      tx += p.y;
+    }
+    w[i] = tw;
+    ax[i] = tx;
+    const double y = b[i] - tx;
+    Wp += tw * tw;
+    Yp += y * y;
+  }
   const double Wb = block_sum<NT>(Wp, sh);
   const double Yb = block_sum<NT>(Yp, sh);
   if (threadIdx.x == 0) { bpart[blockIdx.x] = Wb; bpart[MAXBLK + blockIdx.x] = Yb; }
@@ -246,9 +276,38 @@ __device__ void passN_finish(Scal* st, TraceRec* tr, double* bpart, int nblk, do
 // n-side: finish s, v (sum of dense panel partials, or read them), V and
 // alpha_x, column scores eps^z_j = s_j^2/gamma_j, keys, L1 histogram.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_nside(const double* __restrict__ part, int P,
-                                             int from_part, int n, double* __restrict__ s,
-                                             double* __restrict__ v,
+// Dense pass T second stage: s_j = sum_p part[p][0][j], v_j likewise, in a
+// fixed order (8 panel groups per column, then the 8 group sums in order).
+__global__ void __launch_bounds__(NT) k_dense_reduceT(const double* __restrict__ part, int P, int n,
+                                                     double* __restrict__ s,
+                                                     double* __restrict__ v, const Scal* st) {
+  if (st->halted) return;
+  __shared__ double rs[8][33], rv[8][33];
+  const int c = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + c;
+  const int pending = st->pending;
+  double a = 0.0, bb = 0.0;
+  if (j < n) {
+    for (int p = g; p < P; p += 8) {
+      const double* q = part + (long long)p * 2 * n + j;
+      a += __ldcg(q);
+      if (pending) bb += __ldcg(q + n);
+    }
+  }
+  rs[g][c] = a;
+  rv[g][c] = bb;
+  __syncthreads();
+  if (g == 0 && j < n) {
+    double ta = 0.0, tb = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { ta += rs[q][c]; tb += rv[q][c]; }
+    s[j] = ta;
+    v[j] = tb;
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_nside(int n, const double* __restrict__ s,
+                                             const double* __restrict__ v,
                                              const double* __restrict__ gamma,
                                              unsigned long long* __restrict__ keys, Scal* st,
                                              TraceRec* tr, unsigned int* gh, double* bpart) {
@@ -262,22 +321,11 @@ __global__ void __launch_bounds__(NT) k_nside(const double* __restrict__ part, i
   const unsigned long long seed = st->seed;
   double Vp = 0.0;
   for (int j = blockIdx.x * NT + threadIdx.x; j < n; j += gridDim.x * NT) {
-    double sj, vj;
-    if (from_part) {
-      sj = 0.0; vj = 0.0;
-      const double* q = part + j;
-      for (int p = 0; p < P; ++p) {
-        sj += __ldcg(q);
-        vj += __ldcg(q + n);
-        q += 2LL * n;
-      }
-      s[j] = sj;
-      v[j] = vj;
-    } else {
-      sj = s[j];
-      vj = v[j];
+    const double sj = s[j];
+    if (pending) {
+      const double vj = v[j];
+      Vp += vj * vj;
     }
-    if (pending) Vp += vj * vj;
     const double g = gamma[j];
     const double eps = g > 0.0 ? __ddiv_rn(__dmul_rn(sj, sj), g) : 0.0;
     const unsigned long long key = make_key(eps, (unsigned long long)j, k, 0u, seed);

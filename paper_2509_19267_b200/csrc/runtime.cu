@@ -58,6 +58,10 @@ struct rgdbek_ctx {
   int* ri = nullptr;
   double* rv = nullptr;
   int vecN = 8, vecT = 8;
+  int passN_grid = MAXBLK;              // dense pass N: resident blocks (occupancy x SMs)
+  int nCH = 0, nQ = 1;                  // dense pass N: column chunk width, chunks per row
+  double* npart = nullptr;              // dense pass N chunk partials [Q][m_loc][2]
+  int graph_mode = 0;                   // 0 = WHILE node, 1 = plain body graph, 2 = eager
   // vectors
   double *b = nullptr, *rho = nullptr, *gamma = nullptr;
   double *x = nullptr, *s = nullptr, *v = nullptr, *zeta = nullptr, *xstar = nullptr;
@@ -275,6 +279,7 @@ void launch_csr_vec(rgdbek_ctx* h, int vec, const long long* ptr, const int* idx
 }
 
 constexpr int PT_TPB = 128;   // dense pass T: threads per block (2 columns each)
+constexpr int PN_ROWS = 2;    // dense pass N: rows per work unit
 
 void launch_passT(rgdbek_ctx* h) {
   if (h->dense) {
@@ -288,12 +293,14 @@ void launch_passT(rgdbek_ctx* h) {
 
 void launch_passN(rgdbek_ctx* h) {
   if (h->dense) {
-    constexpr int ROWS = 2;
-    const long long groups = (h->m_loc + ROWS - 1) / ROWS;
-    const int grid = nblocks(groups, NT / 32, MAXBLK);
-    k_dense_passN<ROWS><<<grid, NT, 0, h->stream>>>(h->A, h->lda, (int)h->m_loc, (int)h->n,
-                                                   h->zeta, h->x, h->b, h->w, h->ax, h->st,
-                                                   h->trace, h->bpart);
+    const long long groups = (h->m_loc + PN_ROWS - 1) / PN_ROWS;
+    const long long units = groups * h->nQ;
+    const int grid = (int)std::min<long long>((units + NT / 32 - 1) / (NT / 32), h->passN_grid);
+    k_dense_passN<PN_ROWS><<<grid, NT, 0, h->stream>>>(h->A, h->lda, (int)h->m_loc, (int)h->n,
+                                                      h->nCH, h->nQ, h->zeta, h->x, h->npart,
+                                                      h->st);
+    k_dense_reduceN<<<nblocks(h->m_loc, NT, MAXBLK), NT, 0, h->stream>>>(
+        h->npart, h->nQ, (int)h->m_loc, h->b, h->w, h->ax, h->st, h->trace, h->bpart);
   } else {
     launch_csr_vec<0>(h, h->vecN, h->rp, h->ci, h->cv, h->m_loc, h->zeta, h->x, h->b, h->w,
                       h->ax);
@@ -310,8 +317,12 @@ long long enqueue_body(rgdbek_ctx* h, cudaGraphConditionalHandle cond, int use_c
   unsigned long long* km = h->keys_m;
   // ---- column step ----
   launch_passT(h); ++L;
-  k_nside<<<gn, NT, 0, h->stream>>>(h->part, h->P, h->dense ? 1 : 0, (int)h->n, h->s, h->v,
-                                    h->gamma, kn, h->st, h->trace, h->hist, h->bpart); ++L;
+  if (h->dense) {
+    k_dense_reduceT<<<nblocks(h->n, 32, 1 << 20), NT, 0, h->stream>>>(h->part, h->P, (int)h->n,
+                                                                      h->s, h->v, h->st); ++L;
+  }
+  k_nside<<<gn, NT, 0, h->stream>>>((int)h->n, h->s, h->v, h->gamma, kn, h->st, h->trace,
+                                    h->hist, h->bpart); ++L;
   k_select_pass<NT, 2><<<gsn, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0, h->hist, h->cand); ++L;
   k_select_pass<NT, 3><<<gsn, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0, h->hist, h->cand); ++L;
   k_select_slow<NT><<<1, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0); ++L;
@@ -320,7 +331,7 @@ long long enqueue_body(rgdbek_ctx* h, cudaGraphConditionalHandle cond, int use_c
   k_mask_n<<<gn, NT, 0, h->stream>>>(kn, h->s, h->v, h->zeta, h->x, h->xstar, nullptr, (int)h->n,
                                      h->st, h->trace, h->bpart); ++L;
   // ---- row step ----
-  launch_passN(h); ++L;
+  launch_passN(h); L += h->dense ? 2 : 1;
   k_mside<<<gm, NT, 0, h->stream>>>((int)h->m_loc, h->row0, h->z, h->w, h->ax, h->b, h->rho,
                                     h->r, km, h->st, h->hist); ++L;
   k_select_pass<NT, 2><<<gsm, NT, 0, h->stream>>>(km, h->m_loc, h->row0, h->st, 1, h->hist,
@@ -335,8 +346,27 @@ long long enqueue_body(rgdbek_ctx* h, cudaGraphConditionalHandle cond, int use_c
 }
 
 rgdbek_status build_graph(rgdbek_ctx* h) {
+  // RGDBEK_GRAPH=plain|eager selects the host-relaunched body graph or plain
+  // stream launches (ncu cannot profile kernels inside conditional graphs).
+  if (const char* gm = getenv("RGDBEK_GRAPH")) {
+    if (!strcmp(gm, "plain")) h->graph_mode = 1;
+    if (!strcmp(gm, "eager")) h->graph_mode = 2;
+  }
+  if (h->graph_mode == 2) {
+    h->use_cond = false;
+    cudaGraphConditionalHandle dummy{};
+    // count launches without enqueueing: capture into a throwaway graph
+    CK(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    h->launches_per_iter = enqueue_body(h, dummy, 0);
+    cudaGraph_t tmp = nullptr;
+    CK(h, cudaStreamEndCapture(h->stream, &tmp));
+    cudaGraphDestroy(tmp);
+    return RGDBEK_OK;
+  }
   // Preferred: graph = WHILE(cond) { body }, the tail kernel sets cond.
   cudaGraph_t g = nullptr;
+  if (h->graph_mode == 1) goto plain;
+  {
   CK(h, cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle cond;
   cudaError_t e = cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault);
@@ -364,6 +394,8 @@ rgdbek_status build_graph(rgdbek_ctx* h) {
       }
     }
   }
+  }
+plain:
   // Fallback: a plain graph of one body, relaunched by the host until halted.
   cudaGetLastError();
   if (g) cudaGraphDestroy(g);
@@ -551,7 +583,15 @@ rgdbek_status run_loop(rgdbek_ctx* h, rgdbek_result* res) {
   } else {
     // host-driven fallback: relaunch the body until the device says halted
     for (;;) {
-      for (int t = 0; t < 8; ++t) CK(h, cudaGraphLaunch(h->body_exec, h->stream));
+      for (int t = 0; t < 8; ++t) {
+        if (h->graph_mode == 2) {
+          cudaGraphConditionalHandle dummy{};
+          enqueue_body(h, dummy, 0);
+          CK(h, cudaGetLastError());
+        } else {
+          CK(h, cudaGraphLaunch(h->body_exec, h->stream));
+        }
+      }
       CK(h, cudaMemcpyAsync(h->st_host, h->st, sizeof(Scal), cudaMemcpyDeviceToHost, h->stream));
       CK(h, cudaStreamSynchronize(h->stream));
       if (h->st_host->halted) break;
@@ -660,6 +700,22 @@ rgdbek_status rgdbek_create_dense(rgdbek_handle* out, int64_t m, int64_t n, cons
   h->R = std::min(h->R, 4096);
   h->P = (int)((h->m_loc + h->R - 1) / h->R);
   if ((s = dalloc(h, &h->part, (size_t)h->P * 2 * h->n)) != RGDBEK_OK) return create_fail(h, s);
+  {
+    int nsm = 148, occ = 1;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dense_passN<PN_ROWS>, NT, 0);
+    h->passN_grid = std::max(1, nsm * std::max(occ, 1));
+    // chunk the columns so every resident warp gets >= ~20 units (balance)
+    const long long warps = (long long)h->passN_grid * (NT / 32);
+    const long long groups = (h->m_loc + PN_ROWS - 1) / PN_ROWS;
+    long long Q = std::max(1LL, (20 * warps + groups - 1) / groups);
+    long long CH = (n + Q - 1) / Q;
+    CH = std::max(256LL, (CH + 63) / 64 * 64);          // whole 512-byte warp rows
+    Q = (n + CH - 1) / CH;
+    h->nCH = (int)CH;
+    h->nQ = (int)Q;
+    if ((s = dalloc(h, &h->npart, (size_t)Q * h->m_loc * 2)) != RGDBEK_OK) return create_fail(h, s);
+  }
   if ((s = finish_create(h)) != RGDBEK_OK) return create_fail(h, s);
   *out = h;
   return RGDBEK_OK;
