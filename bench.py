@@ -223,7 +223,7 @@ def run_ours(args):
 
     # time to tolerance (device time of rgdbek_solve, REL_ERR 1e-6)
     ttt = None
-    if w.xstar is not None and not args.skip_ttt:
+    if w.xstar is not None and w.stop == "rel_err" and not args.skip_ttt:
         s.set_stop("rel_err")
         s.set_reference(w.xstar)
         res = s.solve(1e-6, 100000, 0)

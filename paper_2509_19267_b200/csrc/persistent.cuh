@@ -1,0 +1,762 @@
+// persistent.cuh — the whole RGDBEK iteration loop as ONE persistent kernel.
+//
+// One CTA of PT threads per SM (or fewer for small problems; 1 CTA for C1),
+// all co-resident, separated by a software grid barrier at the ~10 grid-wide
+// dependencies of an iteration (pass T -> scores -> 3 selection levels ->
+// mask -> pass N -> stop test + z update -> 3 levels -> mask).  Every global
+// scalar (V, Z, W, ||b-Ax||^2, X, block sizes, radix buckets) is recomputed
+// redundantly by every CTA from the same per-CTA partials in the same order,
+// so all CTAs take identical decisions without a second barrier; CTA 0 alone
+// writes the Scal state and the trace.  The host launches it once per
+// rgdbek_solve / rgdbek_step call.
+//
+// Same method, same arithmetic and same reduction orders per launch geometry
+// as the multi-kernel graph engine (kernels.cuh); tests run both.
+#pragma once
+#include "kernels.cuh"
+
+namespace rg {
+
+constexpr int PT = 1024;                  // threads per persistent CTA
+constexpr int PW = PT / 32;
+constexpr int ZCH = 1024;                 // rows of z / xi staged per chunk (pass T)
+constexpr int PN_RB = 128;                // rows per batch (dense pass N)
+constexpr int PN_QMAX = 16;               // max column chunks per row (dense pass N)
+
+struct GridBar {
+  unsigned int count;
+  unsigned int pad0[31];
+  unsigned int gen;
+  unsigned int pad1[31];
+};
+
+enum : int { SL_V = 0, SL_Z, SL_R, SL_W, SL_Y, SL_X, SL_NUM };
+
+struct PArgs {
+  int dense, m_loc, n, vecN, vecT, Q, CH;
+  long long row0, lda;
+  const double* A;
+  const long long* rp; const int* ci; const double* cv;
+  const long long* cp; const int* ri; const double* rv;
+  const double *b, *rho, *gamma, *xstar;
+  double *x, *s, *v, *zeta, *z, *w, *ax, *r, *xi;
+  unsigned long long *keys_n, *keys_m;
+  double* part;                     // dense pass T partials [G][2][n]
+  double* bpart;                    // [SL_NUM][G]
+  unsigned int* hist;               // [2 sides][3 levels][NBINS]
+  Cand* cand;                       // [2][CAND_CAP]
+  unsigned long long* acc;          // [2 sides][count, hash]
+  unsigned int* ncand;              // [2]
+  Scal* st;
+  TraceRec* tr;
+  GridBar* bar;
+};
+
+__device__ __forceinline__ void grid_sync(GridBar* gb) {
+  __syncthreads();
+  if (gridDim.x == 1) return;
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vgen = &gb->gen;
+    const unsigned int g = *vgen;
+    __threadfence();
+    const unsigned int t = atomicAdd(&gb->count, 1u);
+    if (t == gridDim.x - 1) {
+      gb->count = 0u;
+      __threadfence();
+      atomicAdd(&gb->gen, 1u);
+    } else {
+      while (*vgen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Block-wide sum of one double per thread, same tree in every CTA.
+__device__ __forceinline__ double pblock_sum(double v, double* sh) {
+  return block_sum<PT>(v, sh);
+}
+
+// Sum over the G per-CTA partials of one slot (identical in every CTA).
+__device__ __forceinline__ double slot_sum(const double* bpart, int slot, double* sh) {
+  double t = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += PT) t += __ldcg(bpart + slot * gridDim.x + i);
+  return pblock_sum(t, sh);
+}
+
+// Bucket holding the need-th (1-based) count of a global histogram.  All
+// threads return (digit, count strictly below).  Redundant in every CTA.
+__device__ void p_find_bucket(const unsigned int* gh, long long need, unsigned int* sh_u,
+                              long long* sh_l, int& digit, long long& below) {
+  constexpr int PER = NBINS / PT;           // 4 bins per thread
+  unsigned int loc[PER];
+  long long mine = 0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    loc[i] = __ldcg(gh + threadIdx.x * PER + i);
+    mine += loc[i];
+  }
+  // inclusive warp scan, then scan of the warp totals
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  long long inc = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) sh_l[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    long long t = sh_l[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long u = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += u;
+    }
+    sh_l[lane] = t;                         // inclusive warp-total scan
+  }
+  __syncthreads();
+  const long long base = inc - mine + (wid > 0 ? sh_l[wid - 1] : 0);
+  if (base < need && need <= base + mine) {
+    long long c = base;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      if (c + loc[i] >= need) {
+        sh_u[0] = threadIdx.x * PER + i;
+        sh_l[32] = c;
+        break;
+      }
+      c += loc[i];
+    }
+  }
+  __syncthreads();
+  digit = (int)sh_u[0];
+  below = sh_l[32];
+  __syncthreads();
+}
+
+// Per-side selection state kept in shared memory (identical in all CTAs).
+struct PSel {
+  unsigned long long prefix, tau;
+  long long below, target, npos, tie;
+  int mode, slow;
+};
+
+// Level-1 finalize: block size clamp and first bucket.
+__device__ void p_sel_level1(PSel* ps, const unsigned int* gh, long long N, long long kblock,
+                             unsigned int* sh_u, long long* sh_l) {
+  const long long never = (long long)__ldcg(gh + (NBINS - 1));
+  const long long npos = N - never;
+  const long long target = kblock < npos ? kblock : npos;
+  int mode = target == 0 ? SEL_NONE : (target == npos ? SEL_ALL : SEL_PENDING);
+  int digit = 0;
+  long long below = 0;
+  if (mode == SEL_PENDING) p_find_bucket(gh, target, sh_u, sh_l, digit, below);
+  if (threadIdx.x == 0) {
+    ps->npos = npos; ps->target = target; ps->mode = mode; ps->slow = 0;
+    ps->prefix = (unsigned long long)digit; ps->below = below;
+    ps->tau = (mode == SEL_ALL) ? KEY_NEVER - 1ull : 0ull;
+    ps->tie = (mode == SEL_ALL) ? 0x7FFFFFFFFFFFFFFFll : -1;
+  }
+  __syncthreads();
+}
+
+// Level 2/3 scan over the keys of the current bucket (grid-stride, all CTAs).
+template <int LEVEL>
+__device__ void p_sel_scan(const PSel* ps, const unsigned long long* __restrict__ keys, long long N,
+                           long long idx_base, unsigned int* gh, Cand* cand, unsigned int* ncand,
+                           unsigned int* h) {
+  if (ps->mode != SEL_PENDING) return;
+  for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
+  __syncthreads();
+  constexpr int SF = (LEVEL == 2) ? L1_SHIFT : L2_SHIFT;
+  constexpr int SD = (LEVEL == 2) ? L2_SHIFT : L3_SHIFT;
+  const unsigned long long pre = ps->prefix;
+  const long long stride = (long long)gridDim.x * PT;
+  for (long long i = (long long)blockIdx.x * PT + threadIdx.x; i < N; i += stride) {
+    const unsigned long long key = keys[i];
+    if ((key >> SF) == pre) {
+      atomicAdd(&h[(key >> SD) & 0xFFFull], 1u);
+      if (LEVEL == 3) {
+        const unsigned int slot = atomicAdd(ncand, 1u);
+        if (slot < CAND_CAP) cand[slot] = Cand{key, idx_base + i};
+      }
+    }
+  }
+  __syncthreads();
+  flush_hist<PT>(h, gh, NBINS);
+}
+
+__device__ void p_sel_level2(PSel* ps, const unsigned int* gh, unsigned int* sh_u, long long* sh_l) {
+  if (ps->mode != SEL_PENDING) return;
+  int digit;
+  long long below;
+  p_find_bucket(gh, ps->target - ps->below, sh_u, sh_l, digit, below);
+  if (threadIdx.x == 0) {
+    ps->prefix = (ps->prefix << 12) | (unsigned long long)digit;
+    ps->below += below;
+  }
+  __syncthreads();
+}
+
+// Slow path (candidate overflow): resolve the rest of the key and the tie index
+// by radix levels over ALL keys, in this CTA alone (redundantly in every CTA).
+__device__ void p_sel_slow(PSel* ps, const unsigned long long* __restrict__ keys, long long N,
+                           long long idx_base, unsigned int* h, unsigned int* sh_u, long long* sh_l) {
+  const int shifts[6] = {16, 4, 0, 20, 8, 0};
+  const unsigned long long masks[6] = {0xFFF, 0xFFF, 0xF, 0xFFF, 0xFFF, 0xFF};
+  unsigned long long kpre = ps->prefix;   // key >> 28
+  int kshift = L3_SHIFT;
+  unsigned long long ipre = 0;
+  int ishift = 32;
+  long long below = ps->below;
+  const long long target = ps->target;
+  for (int lv = 0; lv < 6; ++lv) {
+    for (int q = threadIdx.x; q < NBINS; q += PT) h[q] = 0u;
+    __syncthreads();
+    const bool on_idx = lv >= 3;
+    for (long long i = threadIdx.x; i < N; i += PT) {
+      const unsigned long long key = keys[i];
+      const unsigned long long gi = (unsigned long long)(idx_base + i);
+      const bool in = on_idx ? (key == kpre && (ishift >= 32 || (gi >> ishift) == ipre))
+                             : ((key >> kshift) == kpre);
+      if (in) {
+        const unsigned long long d = on_idx ? ((gi >> shifts[lv]) & masks[lv])
+                                            : ((key >> shifts[lv]) & masks[lv]);
+        atomicAdd(&h[d], 1u);
+      }
+    }
+    __syncthreads();
+    // bucket search on the smem histogram (copy through the helper's global-read path)
+    constexpr int PER = NBINS / PT;
+    long long mine = 0;
+    for (int i = 0; i < PER; ++i) mine += h[threadIdx.x * PER + i];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    long long inc = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) sh_l[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      long long t = sh_l[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long u = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += u;
+      }
+      sh_l[lane] = t;
+    }
+    __syncthreads();
+    const long long need = target - below;
+    const long long base = inc - mine + (wid > 0 ? sh_l[wid - 1] : 0);
+    if (base < need && need <= base + mine) {
+      long long c = base;
+      for (int i = 0; i < PER; ++i) {
+        if (c + h[threadIdx.x * PER + i] >= need) {
+          sh_u[0] = threadIdx.x * PER + i;
+          sh_l[32] = c;
+          break;
+        }
+        c += h[threadIdx.x * PER + i];
+      }
+    }
+    __syncthreads();
+    const unsigned long long dg = sh_u[0];
+    below += sh_l[32];
+    const int bits = (masks[lv] == 0xFFF) ? 12 : (masks[lv] == 0xFF ? 8 : 4);
+    if (!on_idx) {
+      kpre = (kpre << bits) | dg;
+      kshift = shifts[lv];
+    } else {
+      ipre = (ishift >= 32) ? dg : ((ipre << bits) | dg);
+      ishift = shifts[lv];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    ps->tau = kpre;
+    ps->tie = (long long)ipre;
+    ps->mode = SEL_THRESH;
+  }
+  __syncthreads();
+}
+
+// Level-3 finalize + exact rank of the survivors -> (tau, tie).
+__device__ void p_sel_level3(PSel* ps, const unsigned int* gh, const Cand* cand,
+                             const unsigned int* ncand, const unsigned long long* keys, long long N,
+                             long long idx_base, unsigned int* h, unsigned int* sh_u,
+                             long long* sh_l) {
+  if (ps->mode != SEL_PENDING) return;
+  int digit;
+  long long below;
+  p_find_bucket(gh, ps->target - ps->below, sh_u, sh_l, digit, below);
+  __shared__ int nf;
+  if (threadIdx.x == 0) {
+    ps->prefix = (ps->prefix << 12) | (unsigned long long)digit;
+    ps->below += below;
+    nf = 0;
+  }
+  __syncthreads();
+  Cand* fc = reinterpret_cast<Cand*>(h);        // 16 KB = FINAL_CAP survivors
+  const unsigned int nc = __ldcg(ncand);
+  const unsigned long long pre3 = ps->prefix;
+  if (nc <= CAND_CAP) {
+    for (unsigned int c = threadIdx.x; c < nc; c += PT) {
+      const Cand e = cand[c];
+      if ((e.key >> L3_SHIFT) == pre3) {
+        const int sl = atomicAdd(&nf, 1);
+        if (sl < FINAL_CAP) fc[sl] = e;
+      }
+    }
+  }
+  __syncthreads();
+  if (nc > CAND_CAP || nf > FINAL_CAP) {
+    p_sel_slow(ps, keys, N, idx_base, h, sh_u, sh_l);
+    return;
+  }
+  const long long need = ps->target - ps->below;
+  for (int e = threadIdx.x; e < nf; e += PT) {
+    const Cand me = fc[e];
+    long long rank = 0;
+    for (int f = 0; f < nf; ++f) {
+      const Cand o = fc[f];
+      rank += (o.key < me.key) || (o.key == me.key && o.idx < me.idx);
+    }
+    if (rank == need - 1) { ps->tau = me.key; ps->tie = me.idx; }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) ps->mode = SEL_THRESH;
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool p_selected(const PSel* ps, unsigned long long key, long long gidx) {
+  if (ps->mode == SEL_THRESH) return key < ps->tau || (key == ps->tau && gidx <= ps->tie);
+  if (ps->mode == SEL_ALL) return key != KEY_NEVER;
+  return false;
+}
+
+// ---------------------------------------------------------------------------
+// Dense pass T for this CTA's contiguous row range, all columns (column tiles
+// of 2*PT): part[cta][0][j] = sum_i A_ij z_i, part[cta][1][j] = sum_i A_ij xi_i.
+// ---------------------------------------------------------------------------
+__device__ void p_dense_passT(const PArgs& a, int pending, double* zs) {
+  const int G = gridDim.x, bb = blockIdx.x;
+  const int rb = (int)((long long)a.m_loc * bb / G), re = (int)((long long)a.m_loc * (bb + 1) / G);
+  const int ntiles = (a.n + 2 * PT - 1) / (2 * PT);
+  double* out = a.part + (long long)bb * 2 * a.n;
+  for (int t = 0; t < ntiles; ++t) {
+    const int c = t * 2 * PT + 2 * threadIdx.x;
+    double s0 = 0.0, s1 = 0.0, v0 = 0.0, v1 = 0.0;
+    for (int rc = rb; rc < re; rc += ZCH) {
+      const int rows = min(ZCH, re - rc);
+      __syncthreads();
+      for (int i = threadIdx.x; i < rows; i += PT) {
+        zs[i] = a.z[rc + i];
+        zs[ZCH + i] = pending ? a.xi[rc + i] : 0.0;
+      }
+      __syncthreads();
+      const double* p = a.A + (long long)rc * a.lda + c;
+      if (c + 1 < a.n) {
+#pragma unroll 8
+        for (int i = 0; i < rows; ++i) {
+          const double2 av = ld_stream2(p + (long long)i * a.lda);
+          const double zi = zs[i], xv = zs[ZCH + i];
+          s0 = fma(av.x, zi, s0);
+          s1 = fma(av.y, zi, s1);
+          v0 = fma(av.x, xv, v0);
+          v1 = fma(av.y, xv, v1);
+        }
+      } else if (c < a.n) {
+        for (int i = 0; i < rows; ++i) {
+          const double av = ld_stream(p + (long long)i * a.lda);
+          s0 = fma(av, zs[i], s0);
+          v0 = fma(av, zs[ZCH + i], v0);
+        }
+      }
+    }
+    if (c + 1 < a.n) {
+      out[c] = s0; out[c + 1] = s1;
+      out[a.n + c] = v0; out[a.n + c + 1] = v1;
+    } else if (c < a.n) {
+      out[c] = s0;
+      out[a.n + c] = v0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Dense pass N for this CTA's rows, in batches of PN_RB rows: warp-units of
+// (1 row) x (column chunk of CH), partials in smem, summed in chunk order.
+// Returns this thread's contributions to W and ||b - Ax||^2.
+// ---------------------------------------------------------------------------
+__device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp) {
+  const int G = gridDim.x, bb = blockIdx.x;
+  const int rb = (int)((long long)a.m_loc * bb / G), re = (int)((long long)a.m_loc * (bb + 1) / G);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int Q = a.Q, CH = a.CH, n = a.n;
+  for (int r0 = rb; r0 < re; r0 += PN_RB) {
+    const int rows = min(PN_RB, re - r0);
+    const int units = rows * Q;
+    for (int u = wid; u < units; u += PW) {
+      const int rr = u / Q, q = u - rr * Q;
+      const int c0 = q * CH, c1 = min(n, c0 + CH);
+      const int c1e = c0 + ((c1 - c0) & ~1);
+      const double* arow = a.A + (long long)(r0 + rr) * a.lda;
+      double sw = 0.0, sx = 0.0;
+#pragma unroll 8
+      for (int c = c0 + lane * 2; c < c1e; c += 64) {
+        const double2 zc = __ldg(reinterpret_cast<const double2*>(a.zeta + c));
+        const double2 xc = __ldg(reinterpret_cast<const double2*>(a.x + c));
+        const double2 av = ld_stream2(arow + c);
+        sw = fma(av.x, zc.x, sw); sw = fma(av.y, zc.y, sw);
+        sx = fma(av.x, xc.x, sx); sx = fma(av.y, xc.y, sx);
+      }
+      if (c1e < c1 && lane == 0) {
+        const double av = ld_stream(arow + c1e);
+        sw = fma(av, a.zeta[c1e], sw);
+        sx = fma(av, a.x[c1e], sx);
+      }
+      sw = warp_sum(sw);
+      sx = warp_sum(sx);
+      if (lane == 0) { np[(rr * PN_QMAX + q) * 2] = sw; np[(rr * PN_QMAX + q) * 2 + 1] = sx; }
+    }
+    __syncthreads();
+    if (threadIdx.x < rows) {
+      const int rr = threadIdx.x, i = r0 + rr;
+      double tw = 0.0, tx = 0.0;
+      for (int q = 0; q < Q; ++q) { tw += np[(rr * PN_QMAX + q) * 2]; tx += np[(rr * PN_QMAX + q) * 2 + 1]; }
+      a.w[i] = tw;
+      a.ax[i] = tx;
+      const double y = a.b[i] - tx;
+      Wp += tw * tw;
+      Yp += y * y;
+    }
+    __syncthreads();
+  }
+}
+
+// CSR / CSC dual SpMV over all CTAs' warps (VEC lanes per row).
+template <int VEC>
+__device__ void p_csr_dual(const long long* __restrict__ ptr, const int* __restrict__ idx,
+                           const double* __restrict__ val, int nrows,
+                           const double* __restrict__ in1, const double* __restrict__ in2,
+                           int use2, const double* __restrict__ b, double* __restrict__ out1,
+                           double* __restrict__ out2, double& Wp, double& Yp) {
+  constexpr int SPW = 32 / VEC;
+  const int lane = threadIdx.x & (VEC - 1);
+  const int sub = (threadIdx.x & 31) / VEC;
+  const int gw = (blockIdx.x * PT + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * PT) >> 5;
+  for (int base = gw * SPW; base < nrows; base += nw * SPW) {
+    const int row = base + sub;
+    const bool valid = row < nrows;
+    double a1 = 0.0, a2 = 0.0;
+    if (valid) {
+      const long long p0 = ptr[row], p1 = ptr[row + 1];
+      for (long long p = p0 + lane; p < p1; p += VEC) {
+        const double av = ld_stream(val + p);
+        const int c = __ldg(idx + p);
+        a1 = fma(av, __ldg(in1 + c), a1);
+        if (use2) a2 = fma(av, __ldg(in2 + c), a2);
+      }
+    }
+#pragma unroll
+    for (int o = VEC / 2; o > 0; o >>= 1) {
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o, VEC);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o, VEC);
+    }
+    if (lane == 0 && valid) {
+      out1[row] = a1;
+      out2[row] = a2;
+      if (b) {
+        const double y = b[row] - a2;
+        Wp += a1 * a1;
+        Yp += y * y;
+      }
+    }
+  }
+}
+
+template <int VEC>
+__device__ __forceinline__ void p_csr_dispatch_dummy() {}
+
+__device__ void p_csr(int vec, const long long* ptr, const int* idx, const double* val, int nrows,
+                      const double* in1, const double* in2, int use2, const double* b,
+                      double* o1, double* o2, double& Wp, double& Yp) {
+  switch (vec) {
+    case 2: p_csr_dual<2>(ptr, idx, val, nrows, in1, in2, use2, b, o1, o2, Wp, Yp); break;
+    case 4: p_csr_dual<4>(ptr, idx, val, nrows, in1, in2, use2, b, o1, o2, Wp, Yp); break;
+    case 8: p_csr_dual<8>(ptr, idx, val, nrows, in1, in2, use2, b, o1, o2, Wp, Yp); break;
+    case 16: p_csr_dual<16>(ptr, idx, val, nrows, in1, in2, use2, b, o1, o2, Wp, Yp); break;
+    default: p_csr_dual<32>(ptr, idx, val, nrows, in1, in2, use2, b, o1, o2, Wp, Yp); break;
+  }
+}
+
+// Zero this CTA's slice of one side's histograms / accumulators.
+__device__ void p_zero_side(const PArgs& a, int side) {
+  unsigned int* h = a.hist + side * 3 * NBINS;
+  for (int i = blockIdx.x * PT + threadIdx.x; i < 3 * NBINS; i += gridDim.x * PT) h[i] = 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.acc[2 * side] = 0ull;
+    a.acc[2 * side + 1] = 0ull;
+    a.ncand[side] = 0u;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The persistent kernel.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
+  __shared__ unsigned int h[NBINS];
+  __shared__ double sh[PW];
+  __shared__ unsigned int sh_u[4];
+  __shared__ long long sh_l[40];
+  __shared__ PSel ps;
+  extern __shared__ double dyn[];
+  Scal* st = a.st;
+  TraceRec* tr = a.tr;
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  const int G = gridDim.x;
+  double* bp = a.bpart;
+  // ---- call state (identical in every CTA) ----
+  long long k = st->k;
+  const long long k_begin = st->k_begin, k_end = st->k_end;
+  const double tol = st->tol;
+  const int stop_mode = st->stop_mode, has_ref = st->has_ref;
+  const unsigned long long seed = st->seed;
+  const double bnorm2 = st->bnorm2, xsnorm2 = st->xsnorm2;
+  const long long kc = st->kc, kr = st->kr;
+  int pending = st->pending;
+  double X = st->X;
+  long long kp_prev = st->kp_prev, kpp_prev = st->kpp_prev;
+  const int n = a.n, m_loc = a.m_loc;
+  unsigned int* hn = a.hist;                    // n-side levels 1..3
+  unsigned int* hm = a.hist + 3 * NBINS;        // m-side levels 1..3
+  Cand* cn = a.cand;
+  Cand* cm = a.cand + CAND_CAP;
+
+  for (;;) {
+    // ===== P1: pass T  (s_k = A^T z_k, v_{k-1} = A^T xi_{k-1}) =====
+    double dummyW = 0.0, dummyY = 0.0;
+    if (a.dense) {
+      p_dense_passT(a, pending, dyn);
+    } else {
+      p_csr(a.vecT, a.cp, a.ri, a.rv, n, a.z, a.xi, pending, nullptr, a.s, a.v, dummyW, dummyY);
+    }
+    grid_sync(a.bar);
+    p_zero_side(a, 1);                          // m-side buffers: consumed in P9..P12
+
+    // ===== P2: s, v; V; column scores and keys; level-1 histogram =====
+    for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
+    __syncthreads();
+    double Vp = 0.0;
+    if (a.dense) {
+      const int lane = threadIdx.x & 31;
+      const int gw = (blockIdx.x * PT + threadIdx.x) >> 5, nw = (G * PT) >> 5;
+      for (int j = gw; j < n; j += nw) {
+        double sj = 0.0, vj = 0.0;
+        for (int p = lane; p < G; p += 32) {
+          const double* q = a.part + (long long)p * 2 * n + j;
+          sj += __ldcg(q);
+          if (pending) vj += __ldcg(q + n);
+        }
+        sj = warp_sum(sj);
+        vj = warp_sum(vj);
+        if (lane == 0) {
+          a.s[j] = sj;
+          a.v[j] = vj;
+          if (pending) Vp += vj * vj;
+          const double g = a.gamma[j];
+          const double eps = g > 0.0 ? __ddiv_rn(__dmul_rn(sj, sj), g) : 0.0;
+          const unsigned long long key = make_key(eps, (unsigned long long)j, k, 0u, seed);
+          a.keys_n[j] = key;
+          atomicAdd(&h[key >> L1_SHIFT], 1u);
+        }
+      }
+    } else {
+      for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) {
+        const double sj = a.s[j];
+        if (pending) { const double vj = a.v[j]; Vp += vj * vj; }
+        const double g = a.gamma[j];
+        const double eps = g > 0.0 ? __ddiv_rn(__dmul_rn(sj, sj), g) : 0.0;
+        const unsigned long long key = make_key(eps, (unsigned long long)j, k, 0u, seed);
+        a.keys_n[j] = key;
+        atomicAdd(&h[key >> L1_SHIFT], 1u);
+      }
+    }
+    __syncthreads();
+    flush_hist<PT>(h, hn, NBINS);
+    {
+      const double vb = pblock_sum(Vp, sh);
+      if (threadIdx.x == 0) bp[SL_V * G + blockIdx.x] = vb;
+    }
+    grid_sync(a.bar);
+
+    // ===== P3: V, alpha_x; level-1 bucket (U); level-2 scan =====
+    const double V = slot_sum(bp, SL_V, sh);
+    const int do_x = pending && kpp_prev > 0 && V > 0.0;
+    const double alpha_x = do_x ? __ddiv_rn(X, V) : 0.0;
+    if (lead && pending) {
+      if (TraceRec* t = trace_at(tr, st, k - 1)) t->V = V;
+    }
+    p_sel_level1(&ps, hn, n, kc, sh_u, sh_l);
+    p_sel_scan<2>(&ps, a.keys_n, n, 0, hn + NBINS, cn, a.ncand, h);
+    grid_sync(a.bar);
+
+    // ===== P4: level-2 bucket; level-3 scan + candidates =====
+    p_sel_level2(&ps, hn + NBINS, sh_u, sh_l);
+    p_sel_scan<3>(&ps, a.keys_n, n, 0, hn + 2 * NBINS, cn, a.ncand, h);
+    grid_sync(a.bar);
+
+    // ===== P5: exact threshold; zeta, Z, |U|, hash; x_k = x_{k-1} + alpha_x v =====
+    p_sel_level3(&ps, hn + 2 * NBINS, cn, a.ncand, a.keys_n, n, 0, h, sh_u, sh_l);
+    {
+      double Zp = 0.0, Rp = 0.0;
+      long long cnt = 0;
+      unsigned long long hs = 0ull;
+      for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) {
+        const double sj = a.s[j];
+        const bool sel = p_selected(&ps, a.keys_n[j], j);
+        a.zeta[j] = sel ? sj : 0.0;
+        if (sel) { Zp += sj * sj; cnt += 1; hs += splitmix64((unsigned long long)j); }
+        double xj = a.x[j];
+        if (do_x) { xj = __dadd_rn(xj, __dmul_rn(alpha_x, a.v[j])); a.x[j] = xj; }
+        if (has_ref) { const double d = xj - a.xstar[j]; Rp += d * d; }
+      }
+      cnt = warp_sum_ll(cnt);
+      hs = warp_sum_u64(hs);
+      if ((threadIdx.x & 31) == 0 && (cnt || hs)) {
+        atomicAdd(&a.acc[0], (unsigned long long)cnt);
+        atomicAdd(&a.acc[1], hs);
+      }
+      const double zb = pblock_sum(Zp, sh);
+      const double rb = pblock_sum(Rp, sh);
+      if (threadIdx.x == 0) { bp[SL_Z * G + blockIdx.x] = zb; bp[SL_R * G + blockIdx.x] = rb; }
+    }
+    pending = 0;
+    grid_sync(a.bar);
+
+    // ===== P6: Z, |U|; pass N (w = A zeta, A x_k) with W / ||b - Ax||^2 partials =====
+    const double Z = slot_sum(bp, SL_Z, sh);
+    const double relerr2 = slot_sum(bp, SL_R, sh);
+    const long long kp = (long long)__ldcg(&a.acc[0]);
+    const unsigned long long hashU = __ldcg(&a.acc[1]);
+    if (lead) {
+      if (kp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 1;
+      if (TraceRec* t = trace_at(tr, st, k)) { t->k = k; t->kp = kp; t->hash_u = hashU; t->Z = Z; }
+    }
+    {
+      double Wp = 0.0, Yp = 0.0;
+      if (a.dense) {
+        p_dense_passN(a, dyn, Wp, Yp);
+      } else {
+        p_csr(a.vecN, a.rp, a.ci, a.cv, m_loc, a.zeta, a.x, 1, a.b, a.w, a.ax, Wp, Yp);
+      }
+      const double wb = pblock_sum(Wp, sh);
+      const double yb = pblock_sum(Yp, sh);
+      if (threadIdx.x == 0) { bp[SL_W * G + blockIdx.x] = wb; bp[SL_Y * G + blockIdx.x] = yb; }
+    }
+    grid_sync(a.bar);
+
+    // ===== P8: stop test on x_k; z_{k+1}, r, row scores and keys, level-1 histogram =====
+    const double W = slot_sum(bp, SL_W, sh);
+    const double Y = slot_sum(bp, SL_Y, sh);
+    {
+      const double rse = Y / bnorm2;
+      const double rel = has_ref ? sqrt(relerr2 / xsnorm2) : __longlong_as_double(0x7FF8000000000000ll);
+      int halt = 0, outcome = RGDBEK_MAX_ITER;
+      if (k > k_begin) {
+        if (stop_mode == RGDBEK_STOP_RSE && rse <= tol) { halt = 1; outcome = RGDBEK_CONVERGED; }
+        else if (stop_mode == RGDBEK_STOP_REL_ERR && rel <= tol) { halt = 1; outcome = RGDBEK_CONVERGED; }
+        else if (kp_prev == 0 && kpp_prev == 0) { halt = 1; outcome = RGDBEK_STALLED; }
+      }
+      if (!halt && (k > k_begin || k_end == k_begin) && k >= k_end) { halt = 1; outcome = RGDBEK_MAX_ITER; }
+      if (lead) {
+        if (TraceRec* t = trace_at(tr, st, k)) t->W = W;
+        if (k >= 1) { if (TraceRec* t = trace_at(tr, st, k - 1)) t->rse = rse; }
+      }
+      if (halt) {
+        p_zero_side(a, 0);
+        if (lead) {
+          st->halted = 1; st->outcome = outcome; st->iters = k; st->rse_out = rse;
+          st->relerr_out = rel; st->k = k; st->pending = 0; st->X = X;
+          st->kp_prev = kp_prev; st->kpp_prev = kpp_prev;
+          st->Z = Z; st->W = W; st->Y = Y; st->V = V; st->relerr2 = relerr2;
+        }
+        return;
+      }
+    }
+    for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
+    __syncthreads();
+    {
+      const int doz = kp > 0 && W > 0.0;
+      const double az = doz ? __ddiv_rn(Z, W) : 0.0;
+      for (int i = blockIdx.x * PT + threadIdx.x; i < m_loc; i += G * PT) {
+        double zi = a.z[i];
+        if (doz) { zi = __dsub_rn(zi, __dmul_rn(az, a.w[i])); a.z[i] = zi; }
+        const double ri = __dsub_rn(__dsub_rn(a.b[i], zi), a.ax[i]);
+        a.r[i] = ri;
+        const double p = a.rho[i];
+        const double eps = p > 0.0 ? __ddiv_rn(__dmul_rn(ri, ri), p) : 0.0;
+        const unsigned long long key = make_key(eps, (unsigned long long)(a.row0 + i), k, 1u, seed);
+        a.keys_m[i] = key;
+        atomicAdd(&h[key >> L1_SHIFT], 1u);
+      }
+    }
+    __syncthreads();
+    flush_hist<PT>(h, hm, NBINS);
+    p_zero_side(a, 0);                          // n-side buffers: consumed in P3..P6
+    grid_sync(a.bar);
+
+    // ===== P9: level-1 bucket (J); level-2 scan =====
+    p_sel_level1(&ps, hm, m_loc, kr, sh_u, sh_l);
+    p_sel_scan<2>(&ps, a.keys_m, m_loc, a.row0, hm + NBINS, cm, a.ncand + 1, h);
+    grid_sync(a.bar);
+
+    // ===== P10: level-2 bucket; level-3 scan + candidates =====
+    p_sel_level2(&ps, hm + NBINS, sh_u, sh_l);
+    p_sel_scan<3>(&ps, a.keys_m, m_loc, a.row0, hm + 2 * NBINS, cm, a.ncand + 1, h);
+    grid_sync(a.bar);
+
+    // ===== P11: exact threshold; xi = r on J, X, |J|, hash =====
+    p_sel_level3(&ps, hm + 2 * NBINS, cm, a.ncand + 1, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
+    {
+      double Xp = 0.0;
+      long long cnt = 0;
+      unsigned long long hs = 0ull;
+      for (int i = blockIdx.x * PT + threadIdx.x; i < m_loc; i += G * PT) {
+        const long long gi = a.row0 + i;
+        const bool sel = p_selected(&ps, a.keys_m[i], gi);
+        const double ri = a.r[i];
+        a.xi[i] = sel ? ri : 0.0;
+        if (sel) { Xp += ri * ri; cnt += 1; hs += splitmix64((unsigned long long)gi); }
+      }
+      cnt = warp_sum_ll(cnt);
+      hs = warp_sum_u64(hs);
+      if ((threadIdx.x & 31) == 0 && (cnt || hs)) {
+        atomicAdd(&a.acc[2], (unsigned long long)cnt);
+        atomicAdd(&a.acc[3], hs);
+      }
+      const double xb = pblock_sum(Xp, sh);
+      if (threadIdx.x == 0) bp[SL_X * G + blockIdx.x] = xb;
+    }
+    grid_sync(a.bar);
+
+    // ===== P12: X, |J|; bookkeeping; k++ =====
+    X = slot_sum(bp, SL_X, sh);
+    const long long kpp = (long long)__ldcg(&a.acc[2]);
+    const unsigned long long hashJ = __ldcg(&a.acc[3]);
+    if (lead) {
+      if (kpp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 2;
+      if (TraceRec* t = trace_at(tr, st, k)) { t->kpp = kpp; t->hash_j = hashJ; t->X = X; }
+    }
+    kp_prev = kp;
+    kpp_prev = kpp;
+    pending = 1;
+    k += 1;
+    __syncthreads();
+  }
+}
+
+}  // namespace rg

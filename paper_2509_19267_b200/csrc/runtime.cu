@@ -19,7 +19,7 @@
 #include <string>
 #include <vector>
 
-#include "kernels.cuh"
+#include "persistent.cuh"
 
 using namespace rg;
 
@@ -62,6 +62,15 @@ struct rgdbek_ctx {
   int nCH = 0, nQ = 1;                  // dense pass N: column chunk width, chunks per row
   double* npart = nullptr;              // dense pass N chunk partials [Q][m_loc][2]
   int graph_mode = 0;                   // 0 = WHILE node, 1 = plain body graph, 2 = eager
+  int engine = 0;                       // 0 = persistent cooperative kernel, 1 = graph engine
+  int pG = 1;                           // persistent: CTAs
+  size_t p_dyn = 0;                     // persistent: dynamic smem bytes
+  PArgs pargs;                          // persistent: kernel arguments
+  unsigned int* phist = nullptr;        // persistent: [2][3][NBINS]
+  Cand* pcand = nullptr;                // persistent: [2][CAND_CAP]
+  unsigned long long* pacc = nullptr;   // persistent: [4]
+  unsigned int* pncand = nullptr;       // persistent: [2]
+  GridBar* pbar = nullptr;
   // vectors
   double *b = nullptr, *rho = nullptr, *gamma = nullptr;
   double *x = nullptr, *s = nullptr, *v = nullptr, *zeta = nullptr, *xstar = nullptr;
@@ -408,6 +417,67 @@ plain:
   return RGDBEK_OK;
 }
 
+// Persistent engine: geometry, buffers and the kernel argument block.
+rgdbek_status setup_persistent(rgdbek_ctx* h) {
+  if (const char* e = getenv("RGDBEK_ENGINE")) {
+    if (!strcmp(e, "graph")) h->engine = 1;
+  }
+  int nsm = 148, occ = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
+  h->p_dyn = std::max<size_t>(2 * ZCH * sizeof(double), (size_t)PN_RB * PN_QMAX * 2 * sizeof(double));
+  CK(h, cudaFuncSetAttribute(k_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->p_dyn));
+  CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persistent, PT, h->p_dyn));
+  if (occ < 1) return set_err(h, RGDBEK_E_CUDA, "persistent kernel cannot be resident (occupancy 0)");
+  // CTAs: about one per MB of per-iteration traffic, at most one per SM
+  const double bytes = h->dense ? 16.0 * (double)h->m_loc * (double)h->n
+                                : 24.0 * (double)h->nnz + 100.0 * (double)(h->m_loc + h->n);
+  long long G = (long long)std::ceil(bytes / (1 << 20));
+  if (const char* e = getenv("RGDBEK_GRID")) G = atoll(e);
+  G = std::max(1LL, std::min<long long>(G, (long long)nsm * occ));
+  G = std::min<long long>(G, MAXBLK);
+  h->pG = (int)G;
+  TRY(dalloc(h, &h->phist, 6 * NBINS));
+  TRY(dalloc(h, &h->pcand, 2 * CAND_CAP));
+  TRY(dalloc(h, &h->pacc, 4));
+  TRY(dalloc(h, &h->pncand, 2));
+  TRY(dalloc(h, &h->pbar, 1));
+  CK(h, cudaMemsetAsync(h->phist, 0, 6 * NBINS * sizeof(unsigned int), h->stream));
+  CK(h, cudaMemsetAsync(h->pacc, 0, 4 * sizeof(unsigned long long), h->stream));
+  CK(h, cudaMemsetAsync(h->pncand, 0, 2 * sizeof(unsigned int), h->stream));
+  CK(h, cudaMemsetAsync(h->pbar, 0, sizeof(GridBar), h->stream));
+  double* ppart = h->part;
+  if (h->dense && G > h->P) TRY(dalloc(h, &ppart, (size_t)G * 2 * h->n));
+  // dense pass N chunking: ~16 warp-units per warp within a CTA's row batch
+  int Q = 1, CH = (int)h->n;
+  if (h->dense) {
+    const long long rows = std::max<long long>(1, std::min<long long>(PN_RB, (h->m_loc + G - 1) / G));
+    long long q = std::max<long long>(1, std::min<long long>(PN_QMAX, (16 * PW + rows - 1) / rows));
+    long long ch = (h->n + q - 1) / q;
+    ch = std::max<long long>(64, (ch + 63) / 64 * 64);
+    q = (h->n + ch - 1) / ch;
+    Q = (int)q; CH = (int)ch;
+  }
+  PArgs& a = h->pargs;
+  memset(&a, 0, sizeof a);
+  a.dense = h->dense ? 1 : 0; a.m_loc = (int)h->m_loc; a.n = (int)h->n;
+  a.vecN = h->vecN; a.vecT = h->vecT; a.Q = Q; a.CH = CH;
+  a.row0 = h->row0; a.lda = h->lda; a.A = h->A;
+  a.rp = h->rp; a.ci = h->ci; a.cv = h->cv; a.cp = h->cp; a.ri = h->ri; a.rv = h->rv;
+  a.b = h->b; a.rho = h->rho; a.gamma = h->gamma; a.xstar = h->xstar;
+  a.x = h->x; a.s = h->s; a.v = h->v; a.zeta = h->zeta; a.z = h->z; a.w = h->w; a.ax = h->ax;
+  a.r = h->r; a.xi = h->xi; a.keys_n = h->keys_n; a.keys_m = h->keys_m;
+  a.part = ppart; a.bpart = h->bpart; a.hist = h->phist; a.cand = h->pcand; a.acc = h->pacc;
+  a.ncand = h->pncand; a.st = h->st; a.tr = h->trace; a.bar = h->pbar;
+  return RGDBEK_OK;
+}
+
+rgdbek_status launch_persistent(rgdbek_ctx* h) {
+  void* args[] = {(void*)&h->pargs};
+  CK(h, cudaLaunchCooperativeKernel((const void*)k_persistent, dim3(h->pG), dim3(PT), args,
+                                    h->p_dyn, h->stream));
+  return RGDBEK_OK;
+}
+
 rgdbek_status finish_create(rgdbek_ctx* h) {
   // norms of b, block sizes (reading R2), scalar state, graph
   std::vector<double> hb(h->m_loc);
@@ -437,6 +507,7 @@ rgdbek_status finish_create(rgdbek_ctx* h) {
   CK(h, cudaStreamSynchronize(h->stream));
   CK(h, cudaEventCreate(&h->ev0));
   CK(h, cudaEventCreate(&h->ev1));
+  TRY(setup_persistent(h));
   TRY(build_graph(h));
   CK(h, cudaStreamSynchronize(h->stream));
   return RGDBEK_OK;
@@ -578,7 +649,9 @@ rgdbek_status ensure_usable(rgdbek_ctx* h) {
 
 rgdbek_status run_loop(rgdbek_ctx* h, rgdbek_result* res) {
   CK(h, cudaEventRecord(h->ev0, h->stream));
-  if (h->use_cond) {
+  if (h->engine == 0) {
+    TRY(launch_persistent(h));
+  } else if (h->use_cond) {
     CK(h, cudaGraphLaunch(h->exec, h->stream));
   } else {
     // host-driven fallback: relaunch the body until the device says halted

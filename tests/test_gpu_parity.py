@@ -71,6 +71,18 @@ def test_dense_50_iterations(name, eta):
     _run_parity(w, 50, seed=3)
 
 
+@pytest.mark.parametrize("engine,grid", [("graph", None), ("persistent", "1"), ("persistent", "7")])
+@pytest.mark.parametrize("name", ["C1", "C2si", "C3s", "C5t"])
+def test_engines_and_grid_sizes(name, engine, grid, monkeypatch):
+    """Both engines (multi-kernel CUDA graph, persistent cooperative kernel) and
+    persistent grids of 1 and 7 CTAs give the oracle's trajectory."""
+    from workloads import by_name
+    monkeypatch.setenv("RGDBEK_ENGINE", engine)
+    if grid:
+        monkeypatch.setenv("RGDBEK_GRID", grid)
+    _run_parity(by_name(name), 20, seed=4)
+
+
 @pytest.mark.parametrize("name", ["C3s", "C4s", "C5t"])
 def test_sparse_50_iterations(name):
     from workloads import by_name
