@@ -112,12 +112,33 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------
-def make_solver(w, device, stream):
+def make_solver(w, device, stream, row_range=None, nccl_comm=None, A_host=None, b_host=None):
+    """The C-ABI solver for workload w (this rank's rows when row_range is given)."""
     from paper_2509_19267_b200 import Solver
+    from paper_2509_19267_b200.dist import shard_csr
     if w.dense:
-        return Solver(w.A, w.b, eta=w.eta, device=device, stream=stream)
-    return Solver.from_scipy(w.A, w.b, eta=w.eta, symmetric=w.symmetric, device=device,
-                             stream=stream)
+        A = w.A if A_host is None else A_host
+        b = w.b if b_host is None else b_host
+        if row_range is not None:
+            A, b = A[row_range[0]:row_range[1]], b[row_range[0]:row_range[1]]
+        return Solver(A, b, eta=w.eta, device=device, stream=stream, m=w.shape[0],
+                      row_range=row_range, nccl_comm=nccl_comm)
+    rp, ci, val = w.csr_arrays()
+    b = w.b
+    if row_range is not None:
+        rp, ci, val = shard_csr(rp, ci, val, *row_range)
+        b = b[row_range[0]:row_range[1]]
+    return Solver.from_csr(w.shape[0], w.shape[1], rp, ci, val, b, eta=w.eta,
+                           symmetric=w.symmetric and row_range is None, device=device,
+                           stream=stream, row_range=row_range, nccl_comm=nccl_comm)
+
+
+def iteration_bytes(w):
+    """Algorithmic bytes of one iteration: both reads of A + 32 B/row + 24 B/col."""
+    m, n = w.shape
+    a = 8.0 * m * n if w.dense else 12.0 * w.A.nnz + 4.0 * (m + 1)
+    a_t = a if (w.dense or w.symmetric) else 12.0 * w.A.nnz + 4.0 * (n + 1)
+    return a + a_t + 32.0 * m + 24.0 * n
 
 
 def time_kernel(s, kernel, reps, torch):
@@ -177,9 +198,16 @@ def run_ours(args):
     w = by_name(args.workload)
     m, n = w.shape
     stream = torch.cuda.current_stream()
-    # Multi-GPU: this build runs independent replicas per rank; the
-    # row-sharded NCCL plan is selected with --shard once available.
-    s = make_solver(w, local, stream.cuda_stream)
+    comm, rows = None, None
+    if world > 1:
+        # row-sharded solve of ONE system (strong scaling): nnz-balanced row blocks
+        # (P:443), [A_p^T z_p | A_p^T xi_p | X_p] and a few small allreduces per iteration
+        from paper_2509_19267_b200.dist import init_nccl_comm, partition_rows
+        parts = partition_rows(m if w.dense else w.A.indptr, world)
+        rows = parts[rank]
+        comm = init_nccl_comm(local)
+    s = make_solver(w, local, stream.cuda_stream, rows, comm)
+    engine, ctas = s.engine_info()
     s.reset(0)
     s.step(args.warmup)                              # W untimed warm-up iterations
     s.reset(0)
@@ -199,27 +227,40 @@ def run_ours(args):
         tt = torch.tensor([t], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
-    value = args.steps * world / t
-    launches = 1 + s.launches_per_iteration() * (args.steps + 1)
+    value = args.steps / t                           # iterations of the one (sharded) system
+    launches = 1 + (1 if engine == 0 else s.launches_per_iteration() * (args.steps + 1))
 
-    # dominant kernels timed alone (roofline)
+    # roofline of the dominant kernel.  Persistent engine: the timed region IS one
+    # launch of k_persistent (K iterations); achieved = K * B_iter / event time.
     peak, peak_src = load_peaks()
+    b_iter = iteration_bytes(w)
     kernels = {}
     for kid, kname in ((0, "passT"), (1, "passN")):
         dt, bytes_per = time_kernel(s, kid, 20, torch)
         kernels[kname] = {"seconds": dt, "bytes": bytes_per, "gbs": bytes_per / dt / 1e9}
     s.reset(0)
-    dom = max(kernels, key=lambda k: kernels[k]["seconds"])
-    kd = kernels[dom]
-    traffic = load_traffic(args.workload, dom)
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(kd["gbs"], 1),
-                "peak": peak, "unit": "GB/s", "frac": round(kd["gbs"] / peak, 4),
-                "traffic": traffic, "peak_source": peak_src,
-                "kernels": {k: {"achieved": round(v["gbs"], 1), "frac": round(v["gbs"] / peak, 4),
-                                "us_per_launch": round(v["seconds"] * 1e6, 2),
-                                "algorithmic_bytes": v["bytes"]} for k, v in kernels.items()},
-                "iteration_frac": round(sum(v["bytes"] for v in kernels.values())
-                                        * value / world / 1e9 / peak, 4)}
+    tr = load_traffic(args.workload, "k_persistent_per_iter")
+    if engine == 0:
+        ach = b_iter * args.steps / t / 1e9 / world
+        roofline = {"bound": "hbm", "kernel": f"k_persistent ({ctas} CTAs x 1024 threads; "
+                                              f"{args.steps} iterations per launch)",
+                    "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(ach / peak, 4),
+                    "traffic": (tr * (args.steps + 0.6)) if tr else None,
+                    "algorithmic_bytes_per_launch": b_iter * args.steps,
+                    "peak_source": peak_src}
+    else:
+        dom = max(kernels, key=lambda k: kernels[k]["seconds"])
+        kd = kernels[dom]
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": round(kd["gbs"], 1),
+                    "peak": peak, "unit": "GB/s", "frac": round(kd["gbs"] / peak, 4),
+                    "traffic": load_traffic(args.workload, dom), "peak_source": peak_src}
+    roofline["standalone_kernels"] = {
+        k: {"achieved": round(v["gbs"], 1), "frac": round(v["gbs"] / peak, 4),
+            "us_per_launch": round(v["seconds"] * 1e6, 2), "algorithmic_bytes": v["bytes"]}
+        for k, v in kernels.items()}
+    roofline["iteration_bytes"] = b_iter
+    roofline["iteration_frac"] = round(b_iter * value / world / 1e9 / peak, 4)
 
     # time to tolerance (device time of rgdbek_solve, REL_ERR 1e-6)
     ttt = None
@@ -242,11 +283,8 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        if w.dense:
-            from paper_2509_19267_b200 import Solver
-            s2 = Solver(A_h, b_h, eta=w.eta, device=local, stream=stream.cuda_stream)
-        else:
-            s2 = make_solver(w, local, stream.cuda_stream)
+        s2 = make_solver(w, local, stream.cuda_stream, rows, comm,
+                         A_host=A_h if w.dense else None, b_host=b_h)
         s2.reset(0)
         s2.step(args.steps)
         s2.x(out=x_h)
@@ -257,10 +295,29 @@ def run_ours(args):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_e2e = float(tt.item())
         a_bytes = (m * n * 8) if w.dense else (w.A.nnz * 12 + (m + 1) * 8)
-        e2e = {"value": round(args.steps * world / t_e2e, 3), "unit": UNIT,
+        e2e = {"value": round(args.steps / t_e2e, 3), "unit": UNIT,
                "h2d_bytes_per_step": int((a_bytes + 8 * m) / args.steps),
                "d2h_bytes_per_step": int(8 * n / args.steps),
                "note": "create() from pinned host A,b + K iterations + get_x to host; host clock"}
+
+    # per-phase device time of the persistent kernel (separate instrumented handle)
+    phases = None
+    if engine == 0 and world == 1 and not args.skip_phases:
+        os.environ["RGDBEK_PHASE_TIMING"] = "1"
+        sp = make_solver(w, local, stream.cuda_stream)
+        del os.environ["RGDBEK_PHASE_TIMING"]
+        sp.reset(0)
+        kph = min(args.steps, 300)
+        sp.step(kph)
+        names = {1: "passT", 2: "s_v_colkeys", 3: "colsel_L2", 4: "colsel_L3",
+                 5: "colsel_mask_x", 6: "passN", 7: "stop_z_rowkeys", 8: "rowsel_L2",
+                 9: "rowsel_L3", 10: "rowsel_mask", 0: "bookkeeping"}
+        pt = sp.phase_times()
+        phases = {names[i]: round(pt[i] / 1e3 / (kph + 1), 2) for i in names}
+        sp.close()
+    if comm is not None:
+        from paper_2509_19267_b200.dist import destroy_nccl_comm
+        destroy_nccl_comm(comm)
 
     out = None
     if rank == 0:
@@ -274,15 +331,17 @@ def run_ours(args):
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * t / args.steps, 5),
-            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.workload, "description": WORKLOADS.get(args.workload),
                        "m": m, "n": n, "nnz": int(w.nnz), "eta": w.eta,
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "parallelism": f"rows{world} (NCCL)" if world > 1 else "single",
+                       "engine": "persistent" if engine == 0 else "graph",
                        "l2": "inputs larger than L2 (A = %.0f MB > 126 MB)" % (
                            (m * n * 8 if w.dense else w.A.nnz * 12) / 1e6)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "time_to_tol": ttt,
             "gpu_launches": launches, "clocks": clk.summary(),
+            "phases_us_per_iter": phases,
         }
         print(json.dumps(out), flush=True)
     if dist:
@@ -346,6 +405,7 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-ttt", action="store_true")
+    ap.add_argument("--skip-phases", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rule)")

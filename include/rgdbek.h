@@ -174,6 +174,17 @@ rgdbek_status rgdbek_launch_kernel(rgdbek_handle h, int32_t kernel, int32_t reps
 /* Kernels launched per iteration body (for the bench's gpu_launches count). */
 rgdbek_status rgdbek_launches_per_iteration(rgdbek_handle h, int64_t* out);
 
+/* Diagnostics.  rgdbek_phase_times: accumulated device time (ns, %globaltimer read by CTA 0
+ * after each grid barrier) of the persistent engine's phases 0..15, when the handle was
+ * created with RGDBEK_PHASE_TIMING=1 in the environment; *n_out = 0 otherwise.
+ * Phase ids: 1 pass T, 2 s/v + column keys, 3-4 column selection levels, 5 mask + x update,
+ * 6 pass N, 7 stop test + z update + row keys, 8-9 row selection levels, 10 row mask,
+ * 0 bookkeeping.  rgdbek_engine_info: engine 0 = persistent kernel (ctas = its grid),
+ * 1 = multi-kernel CUDA graph (RGDBEK_ENGINE=graph). */
+rgdbek_status rgdbek_phase_times(rgdbek_handle h, double* out_ns, int32_t max_phases,
+                                 int32_t* n_out);
+rgdbek_status rgdbek_engine_info(rgdbek_handle h, int32_t* engine, int32_t* ctas);
+
 /* The cudaStream_t the handle runs on (for events / synchronisation). */
 void*         rgdbek_stream(rgdbek_handle h);
 

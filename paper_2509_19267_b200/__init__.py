@@ -140,6 +140,14 @@ class Solver:
     def launch_kernel(self, kernel, reps):
         return N.rgdbek_launch_kernel(self._h, int(kernel), int(reps))
 
+    def phase_times(self):
+        """Per-phase device ns of the persistent engine (RGDBEK_PHASE_TIMING=1), else []."""
+        return N.rgdbek_phase_times(self._h)
+
+    def engine_info(self):
+        """(engine, ctas): engine 0 = persistent kernel, 1 = CUDA-graph engine."""
+        return N.rgdbek_engine_info(self._h)
+
     def launches_per_iteration(self):
         return N.rgdbek_launches_per_iteration(self._h)
 

@@ -22,6 +22,7 @@ EXPORTED = [
     "rgdbek_reset", "rgdbek_step", "rgdbek_solve", "rgdbek_set_stop", "rgdbek_set_reference",
     "rgdbek_get_x", "rgdbek_get_z", "rgdbek_get_blocks", "rgdbek_get_trace", "rgdbek_set_state",
     "rgdbek_launch_kernel", "rgdbek_launches_per_iteration", "rgdbek_stream",
+    "rgdbek_phase_times", "rgdbek_engine_info",
     "rgdbek_nccl_unique_id", "rgdbek_nccl_comm_init", "rgdbek_nccl_comm_destroy",
     "rgdbek_last_error", "rgdbek_destroy",
 ]
@@ -89,6 +90,9 @@ def load(path=None):
         "rgdbek_launch_kernel": (C.c_int, [H, C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
         "rgdbek_launches_per_iteration": (C.c_int, [H, C.POINTER(C.c_int64)]),
         "rgdbek_stream": (C.c_void_p, [H]),
+        "rgdbek_phase_times": (C.c_int, [H, C.POINTER(C.c_double), C.c_int32,
+                                         C.POINTER(C.c_int32)]),
+        "rgdbek_engine_info": (C.c_int, [H, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "rgdbek_nccl_unique_id": (C.c_int, [P]),
         "rgdbek_nccl_comm_init": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, P,
                                             C.c_int32]),
@@ -202,6 +206,19 @@ def rgdbek_launches_per_iteration(h):
 
 def rgdbek_stream(h):
     return load().rgdbek_stream(h)
+
+
+def rgdbek_phase_times(h):
+    buf = (C.c_double * 16)()
+    cnt = C.c_int32()
+    check(load().rgdbek_phase_times(h, buf, 16, C.byref(cnt)), h)
+    return [buf[i] for i in range(cnt.value)]
+
+
+def rgdbek_engine_info(h):
+    e, c = C.c_int32(), C.c_int32()
+    check(load().rgdbek_engine_info(h, C.byref(e), C.byref(c)), h)
+    return e.value, c.value
 
 
 def rgdbek_nccl_unique_id():

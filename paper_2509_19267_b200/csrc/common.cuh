@@ -45,7 +45,7 @@ struct SelState {
 
 // Last-block counters
 enum : int { C_NSIDE = 0, C_SEL2N, C_SEL3N, C_MASKN, C_PASSN, C_MSIDE, C_SEL2M, C_SEL3M,
-             C_MASKM, C_NUM };
+             C_MASKM, C_SURV, C_NUM };
 
 struct Scal {
   // call control
@@ -66,7 +66,16 @@ struct Scal {
   long long trace_cap;
   SelState seln, selm;
   unsigned int counters[C_NUM];
+  // multi-GPU (row-sharded, graph engine): rank-local partials that are
+  // allreduced in place by NCCL between kernels
+  int dist, pad1;
+  long long m_global;
+  double wy[2];                  // [W_p, ||b_p - A_p x||^2]
+  unsigned long long jacc[2];    // [|J_p|, hash(J_p)]
+  unsigned int nsurv, surv_over; // local survivors of the level-3 bucket
 };
+
+constexpr int SURV_CAP = 256;    // per-rank survivors exchanged by allgather
 
 // Read-only / streaming global loads
 __device__ __forceinline__ double2 ld_stream2(const double* p) {

@@ -240,11 +240,8 @@ __global__ void __launch_bounds__(NT) k_csr_dual(const long long* __restrict__ p
   passN_finish(st, tr, bpart, gridDim.x, sh);
 }
 
-// Stop test on x_k (reading R12): run by the last block of pass N.
-__device__ void passN_finish(Scal* st, TraceRec* tr, double* bpart, int nblk, double* sh) {
-  const double W = reduce_partials<NT>(bpart, nblk, sh);
-  const double Y = reduce_partials<NT>(bpart + MAXBLK, nblk, sh);
-  if (threadIdx.x != 0) return;
+// Stop test on x_k (reading R12), given the global W and ||b - A x_k||^2.
+__device__ void passN_decide(Scal* st, TraceRec* tr, double W, double Y) {
   st->W = W;
   st->Y = Y;
   const long long k = st->k;
@@ -270,6 +267,25 @@ __device__ void passN_finish(Scal* st, TraceRec* tr, double* bpart, int nblk, do
     st->rse_out = rse;
     st->relerr_out = rel;
   }
+}
+
+// Run by the last block of pass N: single GPU -> stop test now; row-sharded ->
+// publish this rank's partials for the NCCL allreduce (k_passN_decide follows).
+__device__ void passN_finish(Scal* st, TraceRec* tr, double* bpart, int nblk, double* sh) {
+  const double W = reduce_partials<NT>(bpart, nblk, sh);
+  const double Y = reduce_partials<NT>(bpart + MAXBLK, nblk, sh);
+  if (threadIdx.x != 0) return;
+  if (st->dist) {
+    st->wy[0] = W;
+    st->wy[1] = Y;
+    return;
+  }
+  passN_decide(st, tr, W, Y);
+}
+
+__global__ void k_passN_decide(Scal* st, TraceRec* tr) {
+  if (st->halted) return;
+  passN_decide(st, tr, st->wy[0], st->wy[1]);
 }
 
 // ---------------------------------------------------------------------------
@@ -308,11 +324,12 @@ __global__ void __launch_bounds__(NT) k_dense_reduceT(const double* __restrict__
 
 __global__ void __launch_bounds__(NT) k_nside(int n, const double* __restrict__ s,
                                              const double* __restrict__ v,
+                                             const double* __restrict__ xslot,
                                              const double* __restrict__ gamma,
                                              unsigned long long* __restrict__ keys, Scal* st,
                                              TraceRec* tr, unsigned int* gh, double* bpart) {
   if (st->halted) return;
-  __shared__ unsigned int h[NBINS];
+  __shared__ __align__(16) unsigned int h[NBINS];
   __shared__ double sh[NT / 32];
   for (int b = threadIdx.x; b < NBINS; b += NT) h[b] = 0u;
   __syncthreads();
@@ -342,9 +359,11 @@ __global__ void __launch_bounds__(NT) k_nside(int n, const double* __restrict__ 
     st->V = V;
     const int dox = pending && st->kpp_prev > 0 && V > 0.0;
     st->do_x = dox;
-    st->alpha_x = dox ? __ddiv_rn(st->X, V) : 0.0;
+    const double X = *xslot;                 // global ||xi||^2 (allreduced when sharded)
+    st->X = X;
+    st->alpha_x = dox ? __ddiv_rn(X, V) : 0.0;
     if (pending) {
-      if (TraceRec* t = trace_at(tr, st, k - 1)) t->V = V;
+      if (TraceRec* t = trace_at(tr, st, k - 1)) { t->V = V; t->X = X; }
     }
   }
   finalize_level1<NT>(&st->seln, gh, n, st->kc);
@@ -430,7 +449,7 @@ __global__ void __launch_bounds__(NT) k_mside(int m_loc, long long row0, double*
                                              unsigned long long* __restrict__ keys, Scal* st,
                                              unsigned int* gh) {
   if (st->halted) return;
-  __shared__ unsigned int h[NBINS];
+  __shared__ __align__(16) unsigned int h[NBINS];
   for (int q = threadIdx.x; q < NBINS; q += NT) h[q] = 0u;
   __syncthreads();
   const int doz = st->kp > 0 && st->W > 0.0;
@@ -453,6 +472,7 @@ __global__ void __launch_bounds__(NT) k_mside(int m_loc, long long row0, double*
   }
   __syncthreads();
   flush_hist<NT>(h, gh, NBINS);
+  if (st->dist) return;                      // histogram is allreduced, then k_sel_fin
   if (!last_block(&st->counters[C_MSIDE])) return;
   finalize_level1<NT>(&st->selm, gh, m_loc, st->kr);
 }
@@ -460,12 +480,23 @@ __global__ void __launch_bounds__(NT) k_mside(int m_loc, long long row0, double*
 // ---------------------------------------------------------------------------
 // mask m: xi = r on J; X, |J|, hash(J); x-update becomes pending.
 // ---------------------------------------------------------------------------
+__device__ void maskm_finish(Scal* st, TraceRec* tr, long long kpp, unsigned long long hj) {
+  const SelState& ss = st->selm;
+  if (kpp != (ss.mode == SEL_NONE ? 0 : ss.target)) st->error |= 2;
+  st->kpp = kpp;
+  st->hashJ = hj;
+  st->kp_prev = st->kp;
+  st->kpp_prev = kpp;
+  st->pending = 1;
+  if (TraceRec* t = trace_at(tr, st, st->k)) { t->kpp = kpp; t->hash_j = hj; }
+}
+
 __global__ void __launch_bounds__(NT) k_mask_m(const unsigned long long* __restrict__ keys,
                                               const double* __restrict__ r,
                                               double* __restrict__ xi,
                                               unsigned char* __restrict__ selmask, int m_loc,
                                               long long row0, Scal* st, TraceRec* tr,
-                                              double* bpart) {
+                                              double* bpart, double* xslot) {
   if (st->halted) return;
   __shared__ double sh[NT / 32];
   const SelState ss = st->selm;
@@ -499,17 +530,19 @@ __global__ void __launch_bounds__(NT) k_mask_m(const unsigned long long* __restr
     const unsigned long long hj = __ldcg(&st->hash_acc);
     st->cnt_acc = 0;
     st->hash_acc = 0ull;
-    if (kpp != (ss.mode == SEL_NONE ? 0 : ss.target)) st->error |= 2;
-    st->X = X;
-    st->kpp = kpp;
-    st->hashJ = hj;
-    st->kp_prev = st->kp;
-    st->kpp_prev = kpp;
-    st->pending = 1;
-    if (TraceRec* t = trace_at(tr, st, st->k)) {
-      t->kpp = kpp; t->hash_j = hj; t->X = X;
+    *xslot = X;            // rides in the next pass-T allreduce [s | v | X] when sharded
+    if (st->dist) {        // |J|, hash(J) of this rank: allreduced, then k_maskm_finish
+      st->jacc[0] = (unsigned long long)kpp;
+      st->jacc[1] = hj;
+      return;
     }
+    maskm_finish(st, tr, kpp, hj);
   }
+}
+
+__global__ void k_maskm_finish(Scal* st, TraceRec* tr) {
+  if (st->halted) return;
+  maskm_finish(st, tr, (long long)st->jacc[0], st->jacc[1]);
 }
 
 // ---------------------------------------------------------------------------

@@ -22,6 +22,7 @@ constexpr int PW = PT / 32;
 constexpr int ZCH = 1024;                 // rows of z / xi staged per chunk (pass T)
 constexpr int PN_RB = 128;                // rows per batch (dense pass N)
 constexpr int PN_QMAX = 16;               // max column chunks per row (dense pass N)
+constexpr int LOCAL_SEL_MAX = 16384;      // selections over <= this many keys run CTA-locally
 
 struct GridBar {
   unsigned int count;
@@ -50,24 +51,53 @@ struct PArgs {
   Scal* st;
   TraceRec* tr;
   GridBar* bar;
+  unsigned long long* ptime;        // optional per-phase device time (ns), [16]
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Sense-free generation barrier: one acq_rel ticket per CTA, the last arriver
+// resets the count and bumps the generation with a release store; the others
+// spin on an acquire load (no full fences: the release/acquire pair orders
+// every CTA's prior global writes before every CTA's later reads).
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned int atom_add_acqrel_u32(unsigned int* p, unsigned int v) {
+  unsigned int old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 
 __device__ __forceinline__ void grid_sync(GridBar* gb) {
   __syncthreads();
   if (gridDim.x == 1) return;
   if (threadIdx.x == 0) {
-    volatile unsigned int* vgen = &gb->gen;
-    const unsigned int g = *vgen;
-    __threadfence();
-    const unsigned int t = atomicAdd(&gb->count, 1u);
+    const unsigned int g = ld_acquire_u32(&gb->gen);
+    fence_acq_rel_gpu();                    // this CTA's writes (ordered by bar.sync) first
+    const unsigned int t = atom_add_acqrel_u32(&gb->count, 1u);
     if (t == gridDim.x - 1) {
-      gb->count = 0u;
-      __threadfence();
-      atomicAdd(&gb->gen, 1u);
+      gb->count = 0u;                       // ordered before the release below
+      st_release_u32(&gb->gen, g + 1u);
     } else {
-      while (*vgen == g) __nanosleep(20);
+      while (ld_acquire_u32(&gb->gen) == g) { }
     }
-    __threadfence();
+    // gpu-scope fence: also invalidates this SM's L1 (CCTL.IVALL), so the
+    // read-only-path loads (__ldg) of vectors rewritten in earlier phases
+    // (zeta, x, z, xi) see the new values.
+    fence_acq_rel_gpu();
   }
   __syncthreads();
 }
@@ -93,7 +123,7 @@ __device__ void p_find_bucket(const unsigned int* gh, long long need, unsigned i
   long long mine = 0;
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    loc[i] = __ldcg(gh + threadIdx.x * PER + i);
+    loc[i] = gh[threadIdx.x * PER + i];      // smem or global (after a grid barrier)
     mine += loc[i];
   }
   // inclusive warp scan, then scan of the warp totals
@@ -330,6 +360,66 @@ __device__ void p_sel_level3(PSel* ps, const unsigned int* gh, const Cand* cand,
   __syncthreads();
 }
 
+// Small selections (N <= LOCAL_SEL_MAX): after the grid-wide level-1 bucket,
+// every CTA resolves levels 2, 3 and the survivors by itself from all N keys
+// (identical results everywhere), saving two grid barriers.
+__device__ void p_sel_local(PSel* ps, const unsigned long long* __restrict__ keys, long long N,
+                            long long idx_base, unsigned int* h, unsigned int* sh_u,
+                            long long* sh_l) {
+  if (ps->mode != SEL_PENDING) return;
+  __shared__ int nfl;
+  for (int lv = 2; lv <= 3; ++lv) {
+    const int sf = lv == 2 ? L1_SHIFT : L2_SHIFT;
+    const int sd = lv == 2 ? L2_SHIFT : L3_SHIFT;
+    for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
+    __syncthreads();
+    const unsigned long long pre = ps->prefix;
+    for (long long i = threadIdx.x; i < N; i += PT) {
+      const unsigned long long key = keys[i];
+      if ((key >> sf) == pre) atomicAdd(&h[(key >> sd) & 0xFFFull], 1u);
+    }
+    __syncthreads();
+    int digit;
+    long long below;
+    p_find_bucket(h, ps->target - ps->below, sh_u, sh_l, digit, below);
+    if (threadIdx.x == 0) {
+      ps->prefix = (ps->prefix << 12) | (unsigned long long)digit;
+      ps->below += below;
+      nfl = 0;
+    }
+    __syncthreads();
+  }
+  Cand* fc = reinterpret_cast<Cand*>(h);
+  const unsigned long long pre3 = ps->prefix;
+  for (long long i = threadIdx.x; i < N; i += PT) {
+    const unsigned long long key = keys[i];
+    if ((key >> L3_SHIFT) == pre3) {
+      const int sl = atomicAdd(&nfl, 1);
+      if (sl < FINAL_CAP) fc[sl] = Cand{key, idx_base + i};
+    }
+  }
+  __syncthreads();
+  const int nf = nfl;
+  if (nf > FINAL_CAP) {
+    __syncthreads();
+    p_sel_slow(ps, keys, N, idx_base, h, sh_u, sh_l);
+    return;
+  }
+  const long long need = ps->target - ps->below;
+  for (int e = threadIdx.x; e < nf; e += PT) {
+    const Cand me = fc[e];
+    long long rank = 0;
+    for (int f = 0; f < nf; ++f) {
+      const Cand o = fc[f];
+      rank += (o.key < me.key) || (o.key == me.key && o.idx < me.idx);
+    }
+    if (rank == need - 1) { ps->tau = me.key; ps->tie = me.idx; }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) ps->mode = SEL_THRESH;
+  __syncthreads();
+}
+
 __device__ __forceinline__ bool p_selected(const PSel* ps, unsigned long long key, long long gidx) {
   if (ps->mode == SEL_THRESH) return key < ps->tau || (key == ps->tau && gidx <= ps->tie);
   if (ps->mode == SEL_ALL) return key != KEY_NEVER;
@@ -508,7 +598,7 @@ __device__ void p_zero_side(const PArgs& a, int side) {
 // The persistent kernel.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
-  __shared__ unsigned int h[NBINS];
+  __shared__ __align__(16) unsigned int h[NBINS];
   __shared__ double sh[PW];
   __shared__ unsigned int sh_u[4];
   __shared__ long long sh_l[40];
@@ -535,6 +625,14 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
   unsigned int* hm = a.hist + 3 * NBINS;        // m-side levels 1..3
   Cand* cn = a.cand;
   Cand* cm = a.cand + CAND_CAP;
+  unsigned long long t_last = 0;
+#define PH(i)                                                        \
+  if (a.ptime && lead) {                                             \
+    const unsigned long long t_ = gtimer();                          \
+    if (t_last) a.ptime[i] += t_ - t_last;                           \
+    t_last = t_;                                                     \
+  }
+  PH(0);
 
   for (;;) {
     // ===== P1: pass T  (s_k = A^T z_k, v_{k-1} = A^T xi_{k-1}) =====
@@ -545,6 +643,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       p_csr(a.vecT, a.cp, a.ri, a.rv, n, a.z, a.xi, pending, nullptr, a.s, a.v, dummyW, dummyY);
     }
     grid_sync(a.bar);
+    PH(1);
     p_zero_side(a, 1);                          // m-side buffers: consumed in P9..P12
 
     // ===== P2: s, v; V; column scores and keys; level-1 histogram =====
@@ -592,6 +691,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       if (threadIdx.x == 0) bp[SL_V * G + blockIdx.x] = vb;
     }
     grid_sync(a.bar);
+    PH(2);
 
     // ===== P3: V, alpha_x; level-1 bucket (U); level-2 scan =====
     const double V = slot_sum(bp, SL_V, sh);
@@ -601,16 +701,21 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       if (TraceRec* t = trace_at(tr, st, k - 1)) t->V = V;
     }
     p_sel_level1(&ps, hn, n, kc, sh_u, sh_l);
-    p_sel_scan<2>(&ps, a.keys_n, n, 0, hn + NBINS, cn, a.ncand, h);
-    grid_sync(a.bar);
-
-    // ===== P4: level-2 bucket; level-3 scan + candidates =====
-    p_sel_level2(&ps, hn + NBINS, sh_u, sh_l);
-    p_sel_scan<3>(&ps, a.keys_n, n, 0, hn + 2 * NBINS, cn, a.ncand, h);
-    grid_sync(a.bar);
-
-    // ===== P5: exact threshold; zeta, Z, |U|, hash; x_k = x_{k-1} + alpha_x v =====
-    p_sel_level3(&ps, hn + 2 * NBINS, cn, a.ncand, a.keys_n, n, 0, h, sh_u, sh_l);
+    if (n <= LOCAL_SEL_MAX) {
+      p_sel_local(&ps, a.keys_n, n, 0, h, sh_u, sh_l);
+    } else {
+      p_sel_scan<2>(&ps, a.keys_n, n, 0, hn + NBINS, cn, a.ncand, h);
+      grid_sync(a.bar);
+      PH(3);
+      // ===== P4: level-2 bucket; level-3 scan + candidates =====
+      p_sel_level2(&ps, hn + NBINS, sh_u, sh_l);
+      p_sel_scan<3>(&ps, a.keys_n, n, 0, hn + 2 * NBINS, cn, a.ncand, h);
+      grid_sync(a.bar);
+      PH(4);
+      // ===== P5: exact threshold =====
+      p_sel_level3(&ps, hn + 2 * NBINS, cn, a.ncand, a.keys_n, n, 0, h, sh_u, sh_l);
+    }
+    // ===== P5: zeta, Z, |U|, hash; x_k = x_{k-1} + alpha_x v =====
     {
       double Zp = 0.0, Rp = 0.0;
       long long cnt = 0;
@@ -636,6 +741,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     }
     pending = 0;
     grid_sync(a.bar);
+    PH(5);
 
     // ===== P6: Z, |U|; pass N (w = A zeta, A x_k) with W / ||b - Ax||^2 partials =====
     const double Z = slot_sum(bp, SL_Z, sh);
@@ -658,6 +764,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       if (threadIdx.x == 0) { bp[SL_W * G + blockIdx.x] = wb; bp[SL_Y * G + blockIdx.x] = yb; }
     }
     grid_sync(a.bar);
+    PH(6);
 
     // ===== P8: stop test on x_k; z_{k+1}, r, row scores and keys, level-1 histogram =====
     const double W = slot_sum(bp, SL_W, sh);
@@ -708,19 +815,25 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     flush_hist<PT>(h, hm, NBINS);
     p_zero_side(a, 0);                          // n-side buffers: consumed in P3..P6
     grid_sync(a.bar);
+    PH(7);
 
     // ===== P9: level-1 bucket (J); level-2 scan =====
     p_sel_level1(&ps, hm, m_loc, kr, sh_u, sh_l);
-    p_sel_scan<2>(&ps, a.keys_m, m_loc, a.row0, hm + NBINS, cm, a.ncand + 1, h);
-    grid_sync(a.bar);
-
-    // ===== P10: level-2 bucket; level-3 scan + candidates =====
-    p_sel_level2(&ps, hm + NBINS, sh_u, sh_l);
-    p_sel_scan<3>(&ps, a.keys_m, m_loc, a.row0, hm + 2 * NBINS, cm, a.ncand + 1, h);
-    grid_sync(a.bar);
-
-    // ===== P11: exact threshold; xi = r on J, X, |J|, hash =====
-    p_sel_level3(&ps, hm + 2 * NBINS, cm, a.ncand + 1, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
+    if (m_loc <= LOCAL_SEL_MAX) {
+      p_sel_local(&ps, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
+    } else {
+      p_sel_scan<2>(&ps, a.keys_m, m_loc, a.row0, hm + NBINS, cm, a.ncand + 1, h);
+      grid_sync(a.bar);
+      PH(8);
+      // ===== P10: level-2 bucket; level-3 scan + candidates =====
+      p_sel_level2(&ps, hm + NBINS, sh_u, sh_l);
+      p_sel_scan<3>(&ps, a.keys_m, m_loc, a.row0, hm + 2 * NBINS, cm, a.ncand + 1, h);
+      grid_sync(a.bar);
+      PH(9);
+      // ===== P11: exact threshold =====
+      p_sel_level3(&ps, hm + 2 * NBINS, cm, a.ncand + 1, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
+    }
+    // ===== P11: xi = r on J, X, |J|, hash =====
     {
       double Xp = 0.0;
       long long cnt = 0;
@@ -742,6 +855,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       if (threadIdx.x == 0) bp[SL_X * G + blockIdx.x] = xb;
     }
     grid_sync(a.bar);
+    PH(10);
 
     // ===== P12: X, |J|; bookkeeping; k++ =====
     X = slot_sum(bp, SL_X, sh);
@@ -755,8 +869,10 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     kpp_prev = kpp;
     pending = 1;
     k += 1;
+    PH(0);
     __syncthreads();
   }
+#undef PH
 }
 
 }  // namespace rg

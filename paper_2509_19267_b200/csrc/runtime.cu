@@ -71,6 +71,14 @@ struct rgdbek_ctx {
   unsigned long long* pacc = nullptr;   // persistent: [4]
   unsigned int* pncand = nullptr;       // persistent: [2]
   GridBar* pbar = nullptr;
+  // multi-GPU (row-sharded) state
+  int nranks = 1, rank = 0;
+  bool dist = false;
+  double* xslot = nullptr;              // sv + 2n: ||xi||^2 rides in the [s | v | X] allreduce
+  Cand* surv_local = nullptr;           // [SURV_CAP + 1]
+  Cand* surv_all = nullptr;             // [nranks][SURV_CAP + 1]
+  int nccl_fail = 0;
+  unsigned long long* ptime = nullptr;  // persistent: per-phase ns (RGDBEK_PHASE_TIMING=1)
   // vectors
   double *b = nullptr, *rho = nullptr, *gamma = nullptr;
   double *x = nullptr, *s = nullptr, *v = nullptr, *zeta = nullptr, *xstar = nullptr;
@@ -316,6 +324,49 @@ void launch_passN(rgdbek_ctx* h) {
   }
 }
 
+// NCCL entry points, resolved from the libnccl already loaded in the process
+// (torch's), so no second NCCL enters the address space.
+struct NcclApi {
+  typedef int (*allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+  typedef int (*allgather_t)(const void*, void*, size_t, int, void*, cudaStream_t);
+  typedef int (*group_t)();
+  typedef int (*count_t)(void*, int*);
+  allreduce_t allreduce = nullptr;
+  allgather_t allgather = nullptr;
+  group_t gstart = nullptr, gend = nullptr;
+  count_t count = nullptr, rank = nullptr;
+  bool ok = false;
+};
+enum { NCCL_U32 = 3, NCCL_U64 = 5, NCCL_F64 = 8, NCCL_SUM = 0 };
+
+void* nccl_handle() {
+  static void* lib = nullptr;
+  if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  return lib;
+}
+
+NcclApi& nccl_api() {
+  static NcclApi api;
+  if (!api.ok) {
+    void* lib = nccl_handle();
+    if (lib) {
+      api.allreduce = (NcclApi::allreduce_t)dlsym(lib, "ncclAllReduce");
+      api.allgather = (NcclApi::allgather_t)dlsym(lib, "ncclAllGather");
+      api.gstart = (NcclApi::group_t)dlsym(lib, "ncclGroupStart");
+      api.gend = (NcclApi::group_t)dlsym(lib, "ncclGroupEnd");
+      api.count = (NcclApi::count_t)dlsym(lib, "ncclCommCount");
+      api.rank = (NcclApi::count_t)dlsym(lib, "ncclCommUserRank");
+      api.ok = api.allreduce && api.allgather && api.gstart && api.gend && api.count && api.rank;
+    }
+  }
+  return api;
+}
+
+void nccl_allreduce(rgdbek_ctx* h, void* buf, size_t count, int dtype) {
+  if (nccl_api().allreduce(buf, buf, count, dtype, NCCL_SUM, h->nccl, h->stream) != 0) h->nccl_fail = 1;
+}
+
 long long enqueue_body(rgdbek_ctx* h, cudaGraphConditionalHandle cond, int use_cond) {
   long long L = 0;
   const int gn = nblocks(h->n, NT, 1184);
@@ -330,26 +381,53 @@ long long enqueue_body(rgdbek_ctx* h, cudaGraphConditionalHandle cond, int use_c
     k_dense_reduceT<<<nblocks(h->n, 32, 1 << 20), NT, 0, h->stream>>>(h->part, h->P, (int)h->n,
                                                                       h->s, h->v, h->st); ++L;
   }
-  k_nside<<<gn, NT, 0, h->stream>>>((int)h->n, h->s, h->v, h->gamma, kn, h->st, h->trace,
-                                    h->hist, h->bpart); ++L;
+  // sharded rows: [A_p^T z_p | A_p^T xi_p | X_p] summed over ranks in one call
+  if (h->dist) nccl_allreduce(h, h->s, 2 * h->n + 1, NCCL_F64);
+  k_nside<<<gn, NT, 0, h->stream>>>((int)h->n, h->s, h->v, h->xslot, h->gamma, kn, h->st,
+                                    h->trace, h->hist, h->bpart); ++L;
+  // the column selection is replicated: every rank holds the same s
   k_select_pass<NT, 2><<<gsn, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0, h->hist, h->cand); ++L;
   k_select_pass<NT, 3><<<gsn, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0, h->hist, h->cand); ++L;
   k_select_slow<NT><<<1, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0); ++L;
-  // selection masks are kept for rgdbek_get_blocks in a ring of 2 (by k parity):
-  // the parity is read on the device from st->k, so the graph stays static.
   k_mask_n<<<gn, NT, 0, h->stream>>>(kn, h->s, h->v, h->zeta, h->x, h->xstar, nullptr, (int)h->n,
                                      h->st, h->trace, h->bpart); ++L;
   // ---- row step ----
   launch_passN(h); L += h->dense ? 2 : 1;
+  if (h->dist) {
+    nccl_allreduce(h, &h->st->wy[0], 2, NCCL_F64);
+    k_passN_decide<<<1, 1, 0, h->stream>>>(h->st, h->trace); ++L;
+  }
   k_mside<<<gm, NT, 0, h->stream>>>((int)h->m_loc, h->row0, h->z, h->w, h->ax, h->b, h->rho,
                                     h->r, km, h->st, h->hist); ++L;
+  if (h->dist) {
+    nccl_allreduce(h, h->hist, NBINS, NCCL_U32);
+    k_sel_fin<NT><<<1, NT, 0, h->stream>>>(h->st, h->hist, 1); ++L;
+  }
   k_select_pass<NT, 2><<<gsm, NT, 0, h->stream>>>(km, h->m_loc, h->row0, h->st, 1, h->hist,
                                                   h->cand); ++L;
+  if (h->dist) {
+    nccl_allreduce(h, h->hist, NBINS, NCCL_U32);
+    k_sel_fin<NT><<<1, NT, 0, h->stream>>>(h->st, h->hist, 2); ++L;
+  }
   k_select_pass<NT, 3><<<gsm, NT, 0, h->stream>>>(km, h->m_loc, h->row0, h->st, 1, h->hist,
                                                   h->cand); ++L;
-  k_select_slow<NT><<<1, NT, 0, h->stream>>>(km, h->m_loc, h->row0, h->st, 1); ++L;
+  if (h->dist) {
+    nccl_allreduce(h, h->hist, NBINS, NCCL_U32);
+    k_sel_fin<NT><<<1, NT, 0, h->stream>>>(h->st, h->hist, 3); ++L;
+    k_collect_surv<NT><<<gsm, NT, 0, h->stream>>>(km, h->m_loc, h->row0, h->st, h->surv_local); ++L;
+    if (nccl_api().allgather(h->surv_local, h->surv_all, 2 * (SURV_CAP + 1), NCCL_U64, h->nccl,
+                             h->stream) != 0)
+      h->nccl_fail = 1;
+    k_rank_surv<NT><<<1, NT, 0, h->stream>>>(h->st, h->surv_all, h->nranks); ++L;
+  } else {
+    k_select_slow<NT><<<1, NT, 0, h->stream>>>(km, h->m_loc, h->row0, h->st, 1); ++L;
+  }
   k_mask_m<<<gm, NT, 0, h->stream>>>(km, h->r, h->xi, nullptr, (int)h->m_loc, h->row0, h->st,
-                                     h->trace, h->bpart); ++L;
+                                     h->trace, h->bpart, h->xslot); ++L;
+  if (h->dist) {
+    nccl_allreduce(h, &h->st->jacc[0], 2, NCCL_U64);
+    k_maskm_finish<<<1, 1, 0, h->stream>>>(h->st, h->trace); ++L;
+  }
   k_tail<<<1, 1, 0, h->stream>>>(h->st, cond, use_cond); ++L;
   return L;
 }
@@ -468,6 +546,13 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
   a.r = h->r; a.xi = h->xi; a.keys_n = h->keys_n; a.keys_m = h->keys_m;
   a.part = ppart; a.bpart = h->bpart; a.hist = h->phist; a.cand = h->pcand; a.acc = h->pacc;
   a.ncand = h->pncand; a.st = h->st; a.tr = h->trace; a.bar = h->pbar;
+  if (const char* e = getenv("RGDBEK_PHASE_TIMING")) {
+    if (atoi(e)) {
+      TRY(dalloc(h, &h->ptime, 16));
+      CK(h, cudaMemsetAsync(h->ptime, 0, 16 * sizeof(unsigned long long), h->stream));
+      a.ptime = h->ptime;
+    }
+  }
   return RGDBEK_OK;
 }
 
@@ -486,8 +571,16 @@ rgdbek_status finish_create(rgdbek_ctx* h) {
   CK(h, cudaStreamSynchronize(h->stream));
   double bn = 0.0;
   for (double t : hb) bn += t * t;
-  if (h->nccl) {
-    // multi-GPU: the global ||b||^2 is reduced in rgdbek_create_* (see comm.cu)
+  if (h->dist) {
+    // sharded rows: gamma (column norms) and ||b||^2 are sums over ranks
+    double* dbn = nullptr;
+    TRY(dalloc(h, &dbn, 1));
+    CK(h, cudaMemcpyAsync(dbn, &bn, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    nccl_allreduce(h, dbn, 1, NCCL_F64);
+    nccl_allreduce(h, h->gamma, h->n, NCCL_F64);
+    CK(h, cudaMemcpyAsync(&bn, dbn, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (h->nccl_fail) return set_err(h, RGDBEK_E_NCCL, "ncclAllReduce failed at create");
   }
   h->bnorm2 = bn;
   if (!(bn > 0.0)) return set_err(h, RGDBEK_E_ZERO_RHS, "||b|| == 0: RSE is undefined (P:301-304)");
@@ -499,6 +592,8 @@ rgdbek_status finish_create(rgdbek_ctx* h) {
   h->st_host->kr = std::max(1LL, (long long)std::floor(h->eta * (double)h->m + 0.5));
   h->st_host->trace_cap = h->trace_cap;
   h->st_host->stop_mode = h->stop_mode;
+  h->st_host->dist = h->dist ? 1 : 0;
+  h->st_host->m_global = h->m;
   CK(h, cudaMemcpyAsync(h->st, h->st_host, sizeof(Scal), cudaMemcpyHostToDevice, h->stream));
   k_reset_scal<<<1, 1, 0, h->stream>>>(h->st, 0ull, 0);
   k_reset_vecs<<<nblocks(std::max(h->n, h->m_loc), 256, 1184), 256, 0, h->stream>>>(
@@ -509,6 +604,7 @@ rgdbek_status finish_create(rgdbek_ctx* h) {
   CK(h, cudaEventCreate(&h->ev1));
   TRY(setup_persistent(h));
   TRY(build_graph(h));
+  if (h->nccl_fail) return set_err(h, RGDBEK_E_NCCL, "NCCL call failed while capturing the iteration graph");
   CK(h, cudaStreamSynchronize(h->stream));
   return RGDBEK_OK;
 }
@@ -519,8 +615,9 @@ rgdbek_status alloc_vectors(rgdbek_ctx* h) {
   TRY(dalloc(h, &h->rho, m));
   TRY(dalloc(h, &h->gamma, n));
   TRY(dalloc(h, &h->x, n));
-  TRY(dalloc(h, &h->s, n));
-  TRY(dalloc(h, &h->v, n));
+  TRY(dalloc(h, &h->s, 2 * n + 1));      // [s | v | X]: one buffer for the sharded allreduce
+  h->v = h->s + n;
+  h->xslot = h->s + 2 * n;
   TRY(dalloc(h, &h->zeta, n));
   TRY(dalloc(h, &h->xstar, n));
   TRY(dalloc(h, &h->z, m));
@@ -536,7 +633,11 @@ rgdbek_status alloc_vectors(rgdbek_ctx* h) {
   TRY(dalloc(h, &h->trace, std::max<long long>(h->trace_cap, 1)));
   CK(h, cudaMemsetAsync(h->hist, 0, NBINS * sizeof(unsigned int), h->stream));
   CK(h, cudaMemsetAsync(h->xi, 0, m * sizeof(double), h->stream));
-  CK(h, cudaMemsetAsync(h->v, 0, n * sizeof(double), h->stream));
+  CK(h, cudaMemsetAsync(h->s, 0, (2 * n + 1) * sizeof(double), h->stream));
+  if (h->dist) {
+    TRY(dalloc(h, &h->surv_local, SURV_CAP + 1));
+    TRY(dalloc(h, &h->surv_all, (size_t)h->nranks * (SURV_CAP + 1)));
+  }
   CK(h, cudaMemsetAsync(h->xstar, 0, n * sizeof(double), h->stream));
   CK(h, cudaMemsetAsync(h->trace, 0, std::max<long long>(h->trace_cap, 1) * sizeof(TraceRec),
                         h->stream));
@@ -562,8 +663,17 @@ rgdbek_status common_begin(rgdbek_ctx* h, long long m, long long n, const rgdbek
   h->nccl = o->nccl_comm;
   h->trace_cap = std::max(0, o->trace_capacity);
   h->symmetric = o->symmetric != 0;
-  if (h->nccl && (rb != 0 || re != m))
-    return set_err(h, RGDBEK_E_ARG, "multi-GPU sharding is not enabled in this build");
+  if (!h->nccl && (rb != 0 || re != m))
+    return set_err(h, RGDBEK_E_ARG, "a partial row range needs options.nccl_comm");
+  if (h->nccl) {
+    NcclApi& api = nccl_api();
+    if (!api.ok) return set_err(h, RGDBEK_E_NCCL, "libnccl.so.2 not loadable");
+    if (api.count(h->nccl, &h->nranks) != 0 || api.rank(h->nccl, &h->rank) != 0)
+      return set_err(h, RGDBEK_E_NCCL, "ncclCommCount / ncclCommUserRank failed");
+    h->dist = true;
+    h->symmetric = false;   // a row shard's CSC is not its CSR
+    h->engine = 1;          // NCCL calls sit between kernels of the graph engine
+  }
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0)
@@ -1012,6 +1122,26 @@ rgdbek_status rgdbek_launches_per_iteration(rgdbek_handle h, int64_t* out) {
 }
 
 void* rgdbek_stream(rgdbek_handle h) { return h ? (void*)h->stream : nullptr; }
+
+rgdbek_status rgdbek_phase_times(rgdbek_handle h, double* out_ns, int32_t max_phases,
+                                 int32_t* n_out) {
+  TRY(ensure_usable(h));
+  if (!out_ns || !n_out || max_phases < 0) return set_err(h, RGDBEK_E_ARG, "bad arguments");
+  if (!h->ptime || h->engine != 0) { *n_out = 0; return RGDBEK_OK; }
+  unsigned long long t[16];
+  CK(h, cudaMemcpy(t, h->ptime, sizeof t, cudaMemcpyDeviceToHost));
+  const int cnt = std::min(16, (int)max_phases);
+  for (int i = 0; i < cnt; ++i) out_ns[i] = (double)t[i];
+  *n_out = cnt;
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_engine_info(rgdbek_handle h, int32_t* engine, int32_t* ctas) {
+  if (!h || !engine || !ctas) return RGDBEK_E_ARG;
+  *engine = h->engine;
+  *ctas = h->engine == 0 ? h->pG : 0;
+  return RGDBEK_OK;
+}
 
 // NCCL bootstrap: the library dlopen()s the libnccl already loaded in the
 // process (torch's), so no second copy of NCCL enters the address space.

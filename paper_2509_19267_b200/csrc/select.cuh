@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(NT) k_select_pass(const unsigned long long* __
   if (st->halted) return;
   SelState* ss = which ? &st->selm : &st->seln;
   if (ss->mode != SEL_PENDING) return;
-  __shared__ unsigned int h[NBINS];
+  __shared__ __align__(16) unsigned int h[NBINS];
   for (int b = threadIdx.x; b < NBINS; b += NT) h[b] = 0u;
   __syncthreads();
   constexpr int SF = (LEVEL == 2) ? L1_SHIFT : L2_SHIFT;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(NT) k_select_pass(const unsigned long long* __
     const unsigned long long key = keys[i];
     if ((key >> SF) == pre) {
       atomicAdd(&h[(key >> SD) & 0xFFFull], 1u);
-      if (LEVEL == 3) {
+      if (LEVEL == 3 && !(which && st->dist)) {
         const unsigned int slot = atomicAdd(&ss->ncand, 1u);
         if (slot < CAND_CAP) cand[slot] = Cand{key, idx_base + i};
       }
@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(NT) k_select_pass(const unsigned long long* __
   }
   __syncthreads();
   flush_hist<NT>(h, gh, NBINS);
+  if (which && st->dist) return;             // sharded rows: allreduce, then k_sel_fin
   if (!last_block(&st->counters[(LEVEL == 2 ? C_SEL2N : C_SEL3N) + (which ? (C_SEL2M - C_SEL2N) : 0)]))
     return;
   finalize_level<NT>(ss, gh, SD);
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(NT) k_select_slow(const unsigned long long* __
   if (st->halted) return;
   SelState* ss = which ? &st->selm : &st->seln;
   if (ss->mode != SEL_PENDING || !ss->slow) return;
-  __shared__ unsigned int h[NBINS];
+  __shared__ __align__(16) unsigned int h[NBINS];
   __shared__ long long ex[NT];
   __shared__ unsigned long long sel_digit;
   __shared__ long long sel_below;
@@ -249,6 +250,81 @@ __global__ void __launch_bounds__(NT) k_select_slow(const unsigned long long* __
     ss->slow = 0;
     ss->ncand = 0u;
   }
+}
+
+// ---- row-sharded (multi-GPU) selection of J: finalize after each histogram
+// allreduce; the level-3 survivors of every rank are allgathered and ranked.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_sel_fin(Scal* st, unsigned int* gh, int level) {
+  if (st->halted) return;
+  SelState* ss = &st->selm;
+  if (level == 1) {
+    finalize_level1<NT>(ss, gh, st->m_global, st->kr);
+    return;
+  }
+  if (ss->mode != SEL_PENDING) return;
+  finalize_level<NT>(ss, gh, level == 2 ? L2_SHIFT : L3_SHIFT);
+}
+
+// Local keys in the level-3 bucket -> surv[1..], surv[0] = {count, overflow}.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_collect_surv(const unsigned long long* __restrict__ keys,
+                                                     long long N, long long idx_base, Scal* st,
+                                                     Cand* surv) {
+  if (st->halted) return;
+  const SelState& ss = st->selm;
+  if (ss.mode != SEL_PENDING) return;
+  const unsigned long long pre3 = ss.prefix;
+  for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < N; i += (long long)gridDim.x * NT) {
+    const unsigned long long key = keys[i];
+    if ((key >> L3_SHIFT) == pre3) {
+      const unsigned int sl = atomicAdd(&st->nsurv, 1u);
+      if (sl < SURV_CAP) surv[1 + sl] = Cand{key, idx_base + i};
+      else st->surv_over = 1u;
+    }
+  }
+  if (!last_block(&st->counters[C_SURV])) return;
+  if (threadIdx.x == 0) {
+    const unsigned int c = __ldcg(&st->nsurv);
+    surv[0] = Cand{(unsigned long long)(c < SURV_CAP ? c : SURV_CAP), (long long)__ldcg(&st->surv_over)};
+    st->nsurv = 0u;
+    st->surv_over = 0u;
+  }
+}
+
+// Rank the survivors of all ranks (identical on every rank) -> (tau, tie).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_rank_surv(Scal* st, const Cand* __restrict__ all, int P) {
+  if (st->halted) return;
+  SelState* ss = &st->selm;
+  if (ss->mode != SEL_PENDING) return;
+  __shared__ Cand fc[8 * SURV_CAP];
+  __shared__ int nf;
+  if (threadIdx.x == 0) nf = 0;
+  __syncthreads();
+  for (int r = 0; r < P; ++r) {
+    const Cand* blk = all + (long long)r * (SURV_CAP + 1);
+    const int c = (int)blk[0].key;
+    if (blk[0].idx && threadIdx.x == 0) st->error |= 4;     // survivor overflow on a rank
+    for (int e = threadIdx.x; e < c; e += NT) {
+      const int sl = atomicAdd(&nf, 1);
+      if (sl < 8 * SURV_CAP) fc[sl] = blk[1 + e];
+    }
+  }
+  __syncthreads();
+  const int cnt = nf < 8 * SURV_CAP ? nf : 8 * SURV_CAP;
+  const long long need = ss->target - ss->below;
+  for (int e = threadIdx.x; e < cnt; e += NT) {
+    const Cand me = fc[e];
+    long long rank = 0;
+    for (int f = 0; f < cnt; ++f) {
+      const Cand o = fc[f];
+      rank += (o.key < me.key) || (o.key == me.key && o.idx < me.idx);
+    }
+    if (rank == need - 1) { ss->tau = me.key; ss->tie = me.idx; }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) ss->mode = SEL_THRESH;
 }
 
 __device__ __forceinline__ bool is_selected(const SelState& ss, unsigned long long key, long long gidx) {

@@ -274,3 +274,37 @@ def test_full_size_c3_sampled():
     x = s.x()
     assert np.max(np.abs(x[idx] - o.x[idx])) <= 1e-10 * np.max(np.abs(o.x))
     assert np.linalg.norm(s.z() - o.z) <= 1e-10 * np.linalg.norm(w.b)
+
+
+@pytest.mark.parametrize("name", ["C2si", "C5t", "C3s"])
+def test_sharded_code_path_world1_nccl(name):
+    """The row-sharded (NCCL) code path of the library on one GPU: a world of 1
+    rank runs every allreduce / allgather, finalize and survivor kernel of the
+    multi-GPU plan; its trajectory must still be the oracle's."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2509_19267_b200.dist import init_nccl_comm, destroy_nccl_comm
+    from workloads import by_name
+    import bench
+    sock = socket.socket(); sock.bind(("127.0.0.1", 0)); port = sock.getsockname()[1]; sock.close()
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        comm = init_nccl_comm(0)
+        w = by_name(name)
+        s = bench.make_solver(w, 0, None, (0, w.shape[0]), comm)
+        assert s.engine_info()[0] == 1
+        o = _oracle(w)
+        s.reset(2)
+        bn = np.linalg.norm(w.b)
+        for k in range(20):
+            rec = o.iterate(2)
+            s.step(1)
+            g = s.trace()[-1]
+            assert (g["kp"], g["hash_u"], g["kpp"], g["hash_j"]) == (rec.kp, rec.hash_u, rec.kpp, rec.hash_j), k
+            assert np.linalg.norm(s.x() - o.x) <= TOL_X * np.linalg.norm(o.x)
+            assert np.linalg.norm(s.z() - o.z) <= TOL_Z * bn
+        s.close()
+        destroy_nccl_comm(comm)
+    finally:
+        dist.destroy_process_group()
