@@ -20,8 +20,8 @@ namespace rg {
 constexpr int PT = 1024;                  // threads per persistent CTA
 constexpr int PW = PT / 32;
 constexpr int ZCH = 1024;                 // rows of z / xi staged per chunk (pass T)
-constexpr int PN_RB = 128;                // rows per batch (dense pass N)
-constexpr int PN_QMAX = 16;               // max column chunks per row (dense pass N)
+constexpr int PN_RB = 256;                // max rows per batch (dense pass N)
+constexpr int PN_QMAX = 8;                // max column chunks per row (dense pass N)
 constexpr int LOCAL_SEL_MAX = 16384;      // selections over <= this many keys run CTA-locally
 
 struct GridBar {
@@ -485,31 +485,47 @@ __device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp
   const int rb = (int)((long long)a.m_loc * bb / G), re = (int)((long long)a.m_loc * (bb + 1) / G);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int Q = a.Q, CH = a.CH, n = a.n;
-  for (int r0 = rb; r0 < re; r0 += PN_RB) {
-    const int rows = min(PN_RB, re - r0);
-    const int units = rows * Q;
+  const int nbatch = (re - rb + PN_RB - 1) / PN_RB;             // evenly sized batches
+  const int per = nbatch ? (re - rb + nbatch - 1) / nbatch : 0;
+  for (int r0 = rb; r0 < re; r0 += per) {
+    const int rows = min(per, re - r0);
+    const int units = ((rows + 1) >> 1) * Q;                     // 2 rows x 1 chunk per unit
     for (int u = wid; u < units; u += PW) {
-      const int rr = u / Q, q = u - rr * Q;
+      const int rp = u / Q, q = u - rp * Q;
+      const int rr = 2 * rp;
+      const bool two = rr + 1 < rows;
       const int c0 = q * CH, c1 = min(n, c0 + CH);
       const int c1e = c0 + ((c1 - c0) & ~1);
-      const double* arow = a.A + (long long)(r0 + rr) * a.lda;
-      double sw = 0.0, sx = 0.0;
-#pragma unroll 8
+      const double* a0 = a.A + (long long)(r0 + rr) * a.lda;
+      const double* a1 = two ? a0 + a.lda : a0;
+      double w0 = 0.0, x0 = 0.0, w1 = 0.0, x1 = 0.0;
+#pragma unroll 4
       for (int c = c0 + lane * 2; c < c1e; c += 64) {
         const double2 zc = __ldg(reinterpret_cast<const double2*>(a.zeta + c));
         const double2 xc = __ldg(reinterpret_cast<const double2*>(a.x + c));
-        const double2 av = ld_stream2(arow + c);
-        sw = fma(av.x, zc.x, sw); sw = fma(av.y, zc.y, sw);
-        sx = fma(av.x, xc.x, sx); sx = fma(av.y, xc.y, sx);
+        const double2 v0 = ld_stream2(a0 + c);
+        const double2 v1 = two ? ld_stream2(a1 + c) : make_double2(0.0, 0.0);
+        w0 = fma(v0.x, zc.x, w0); w0 = fma(v0.y, zc.y, w0);
+        x0 = fma(v0.x, xc.x, x0); x0 = fma(v0.y, xc.y, x0);
+        w1 = fma(v1.x, zc.x, w1); w1 = fma(v1.y, zc.y, w1);
+        x1 = fma(v1.x, xc.x, x1); x1 = fma(v1.y, xc.y, x1);
       }
       if (c1e < c1 && lane == 0) {
-        const double av = ld_stream(arow + c1e);
-        sw = fma(av, a.zeta[c1e], sw);
-        sx = fma(av, a.x[c1e], sx);
+        const double v0 = ld_stream(a0 + c1e);
+        w0 = fma(v0, a.zeta[c1e], w0);
+        x0 = fma(v0, a.x[c1e], x0);
+        if (two) {
+          const double v1 = ld_stream(a1 + c1e);
+          w1 = fma(v1, a.zeta[c1e], w1);
+          x1 = fma(v1, a.x[c1e], x1);
+        }
       }
-      sw = warp_sum(sw);
-      sx = warp_sum(sx);
-      if (lane == 0) { np[(rr * PN_QMAX + q) * 2] = sw; np[(rr * PN_QMAX + q) * 2 + 1] = sx; }
+      w0 = warp_sum(w0); x0 = warp_sum(x0);
+      w1 = warp_sum(w1); x1 = warp_sum(x1);
+      if (lane == 0) {
+        np[(rr * PN_QMAX + q) * 2] = w0; np[(rr * PN_QMAX + q) * 2 + 1] = x0;
+        if (two) { np[((rr + 1) * PN_QMAX + q) * 2] = w1; np[((rr + 1) * PN_QMAX + q) * 2 + 1] = x1; }
+      }
     }
     __syncthreads();
     if (threadIdx.x < rows) {

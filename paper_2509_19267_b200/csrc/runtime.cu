@@ -529,7 +529,8 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
   int Q = 1, CH = (int)h->n;
   if (h->dense) {
     const long long rows = std::max<long long>(1, std::min<long long>(PN_RB, (h->m_loc + G - 1) / G));
-    long long q = std::max<long long>(1, std::min<long long>(PN_QMAX, (16 * PW + rows - 1) / rows));
+    const long long pairs = (rows + 1) / 2;     // units are 2 rows x 1 chunk
+    long long q = std::max<long long>(1, std::min<long long>(PN_QMAX, (16 * PW + pairs - 1) / pairs));
     long long ch = (h->n + q - 1) / q;
     ch = std::max<long long>(64, (ch + 63) / 64 * 64);
     q = (h->n + ch - 1) / ch;
