@@ -246,7 +246,7 @@ def run_ours(args):
                                               f"{args.steps} iterations per launch)",
                     "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(ach / peak, 4),
-                    "traffic": (tr * (args.steps + 0.6)) if tr else None,
+                    "traffic": (tr * (args.steps + 1)) if tr else None,
                     "algorithmic_bytes_per_launch": b_iter * args.steps,
                     "peak_source": peak_src}
     else:

@@ -1,0 +1,101 @@
+// csr_tiles.cuh — CSR (or CSC) dual SpMV by nnz tiles ("CSR-stream").
+//
+// A sparse pass computes o1 = A in1 and o2 = A in2 over rows (pass N: A zeta,
+// A x; pass T over the CSC: A^T z, A^T xi).  Short rows (5-41 nnz here) make
+// a row-per-thread or sub-warp-per-row loop a chain of three dependent memory
+// round trips per row (row pointer -> value/index -> gathered vector), so
+// each warp keeps almost nothing in flight.  Instead a worker group of TG
+// threads takes a tile of consecutive rows holding <= TILE_NNZ nonzeros:
+//   1. stage the tile's row pointers in shared memory;
+//   2. stream its values and indices with fully coalesced loads (every thread
+//      ~8 independent loads in flight) and store the products val*in1[idx],
+//      val*in2[idx] in shared memory;
+//   3. sum each row's products in order (deterministic) from shared memory.
+// A row longer than TILE_NNZ is a tile by itself, reduced across the group.
+// Tiles are precomputed at create (greedy on the row pointer).
+#pragma once
+#include "common.cuh"
+
+namespace rg {
+
+constexpr int TG = 256;              // threads per worker group
+constexpr int TILE_NNZ = 2048;
+constexpr int TILE_ROWS = 512;
+
+struct TileSmem {
+  double p1[TILE_NNZ];
+  double p2[TILE_NNZ];
+  long long rp[TILE_ROWS + 1];
+  double red[2 * (TG / 32)];
+};
+
+// Barrier over this worker group's TG threads (id 0 == the whole 256-thread block).
+__device__ __forceinline__ void group_bar(int id) {
+  asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(TG) : "memory");
+}
+
+__device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm,
+                          const long long* __restrict__ ptr, const int* __restrict__ idx,
+                          const double* __restrict__ val, const int* __restrict__ tiles,
+                          int ntiles, const double* __restrict__ in1,
+                          const double* __restrict__ in2, int use2,
+                          const double* __restrict__ b, double* __restrict__ o1,
+                          double* __restrict__ o2, double& Wp, double& Yp) {
+  for (int t = gid; t < ntiles; t += ngroups) {
+    const int r0 = tiles[t], r1 = tiles[t + 1];
+    const int nr = r1 - r0;
+    for (int i = lt; i <= nr; i += TG) sm->rp[i] = ptr[r0 + i];
+    group_bar(bar_id);
+    const long long p0 = sm->rp[0], p1 = sm->rp[nr];
+    if (p1 - p0 > TILE_NNZ) {                      // one long row: group-wide reduction
+      double a1 = 0.0, a2 = 0.0;
+      for (long long p = p0 + lt; p < p1; p += TG) {
+        const double a = ld_stream(val + p);
+        const int c = __ldg(idx + p);
+        a1 = fma(a, __ldg(in1 + c), a1);
+        if (use2) a2 = fma(a, __ldg(in2 + c), a2);
+      }
+      a1 = warp_sum(a1);
+      a2 = warp_sum(a2);
+      if ((lt & 31) == 0) { sm->red[2 * (lt >> 5)] = a1; sm->red[2 * (lt >> 5) + 1] = a2; }
+      group_bar(bar_id);
+      if (lt == 0) {
+        double s1 = 0.0, s2 = 0.0;
+        for (int q = 0; q < TG / 32; ++q) { s1 += sm->red[2 * q]; s2 += sm->red[2 * q + 1]; }
+        o1[r0] = s1;
+        o2[r0] = s2;
+        if (b) {
+          const double y = b[r0] - s2;
+          Wp += s1 * s1;
+          Yp += y * y;
+        }
+      }
+      group_bar(bar_id);
+      continue;
+    }
+    const int nz = (int)(p1 - p0);
+#pragma unroll 4
+    for (int q = lt; q < nz; q += TG) {
+      const double a = ld_stream(val + p0 + q);
+      const int c = __ldg(idx + p0 + q);
+      sm->p1[q] = a * __ldg(in1 + c);
+      sm->p2[q] = use2 ? a * __ldg(in2 + c) : 0.0;
+    }
+    group_bar(bar_id);
+    for (int r = lt; r < nr; r += TG) {
+      const int q0 = (int)(sm->rp[r] - p0), q1 = (int)(sm->rp[r + 1] - p0);
+      double s1 = 0.0, s2 = 0.0;
+      for (int q = q0; q < q1; ++q) { s1 += sm->p1[q]; s2 += sm->p2[q]; }
+      o1[r0 + r] = s1;
+      o2[r0 + r] = s2;
+      if (b) {
+        const double y = b[r0 + r] - s2;
+        Wp += s1 * s1;
+        Yp += y * y;
+      }
+    }
+    group_bar(bar_id);
+  }
+}
+
+}  // namespace rg

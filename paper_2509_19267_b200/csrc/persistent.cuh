@@ -52,6 +52,8 @@ struct PArgs {
   TraceRec* tr;
   GridBar* bar;
   unsigned long long* ptime;        // optional per-phase device time (ns), [16]
+  const int* tilesN; const int* tilesT;
+  int ntilesN, ntilesT;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -656,7 +658,10 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     if (a.dense) {
       p_dense_passT(a, pending, dyn);
     } else {
-      p_csr(a.vecT, a.cp, a.ri, a.rv, n, a.z, a.xi, pending, nullptr, a.s, a.v, dummyW, dummyY);
+      const int g = threadIdx.x / TG;
+      csr_tiles(blockIdx.x * (PT / TG) + g, G * (PT / TG), threadIdx.x % TG, 1 + g,
+                reinterpret_cast<TileSmem*>(dyn) + g, a.cp, a.ri, a.rv, a.tilesT, a.ntilesT,
+                a.z, a.xi, pending, nullptr, a.s, a.v, dummyW, dummyY);
     }
     grid_sync(a.bar);
     PH(1);
@@ -773,7 +778,10 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       if (a.dense) {
         p_dense_passN(a, dyn, Wp, Yp);
       } else {
-        p_csr(a.vecN, a.rp, a.ci, a.cv, m_loc, a.zeta, a.x, 1, a.b, a.w, a.ax, Wp, Yp);
+        const int g = threadIdx.x / TG;
+        csr_tiles(blockIdx.x * (PT / TG) + g, G * (PT / TG), threadIdx.x % TG, 1 + g,
+                  reinterpret_cast<TileSmem*>(dyn) + g, a.rp, a.ci, a.cv, a.tilesN, a.ntilesN,
+                  a.zeta, a.x, 1, a.b, a.w, a.ax, Wp, Yp);
       }
       const double wb = pblock_sum(Wp, sh);
       const double yb = pblock_sum(Yp, sh);

@@ -58,6 +58,10 @@ struct rgdbek_ctx {
   int* ri = nullptr;
   double* rv = nullptr;
   int vecN = 8, vecT = 8;
+  int* tilesN = nullptr;                // CSR row tiles (csr_tiles.cuh), [ntilesN + 1]
+  int* tilesT = nullptr;                // CSC row tiles, [ntilesT + 1]
+  int ntilesN = 0, ntilesT = 0;
+  int tile_grid = 1;                    // resident 256-thread tile blocks
   int passN_grid = MAXBLK;              // dense pass N: resident blocks (occupancy x SMs)
   int nCH = 0, nQ = 1;                  // dense pass N: column chunk width, chunks per row
   double* npart = nullptr;              // dense pass N chunk partials [Q][m_loc][2]
@@ -262,6 +266,36 @@ __global__ void k_selmask_to_list(const unsigned char* mask, long long count, lo
     if (mask[i]) out[atomicAdd(pos, 1ull)] = (int)(base + i);
 }
 
+// Greedy row tiles: consecutive rows with <= TILE_NNZ nonzeros and <= TILE_ROWS rows
+// (a longer row is a tile by itself).
+rgdbek_status build_tiles(rgdbek_ctx* h, const long long* d_ptr, long long rows, int** out,
+                          int* nt) {
+  std::vector<long long> rp(rows + 1);
+  CK(h, cudaMemcpyAsync(rp.data(), d_ptr, (rows + 1) * sizeof(long long), cudaMemcpyDeviceToHost,
+                        h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  std::vector<int> t;
+  t.push_back(0);
+  long long start = 0, acc = 0;
+  for (long long r = 0; r < rows; ++r) {
+    const long long len = rp[r + 1] - rp[r];
+    if (r > start && (acc + len > TILE_NNZ || r - start >= TILE_ROWS)) {
+      t.push_back((int)r);
+      start = r;
+      acc = 0;
+    }
+    acc += len;
+  }
+  t.push_back((int)rows);
+  int* d = nullptr;
+  TRY(dalloc(h, &d, t.size()));
+  CK(h, cudaMemcpyAsync(d, t.data(), t.size() * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  *out = d;
+  *nt = (int)t.size() - 1;
+  return RGDBEK_OK;
+}
+
 int pick_vec(double avg) {
   int v = 2;
   while (v < 32 && v < avg) v <<= 1;
@@ -304,7 +338,9 @@ void launch_passT(rgdbek_ctx* h) {
     k_dense_passT<PT_TPB><<<grid, PT_TPB, 2 * h->R * sizeof(double), h->stream>>>(
         h->A, h->lda, (int)h->m_loc, (int)h->n, h->R, h->z, h->xi, h->part, h->st);
   } else {
-    launch_csr_vec<1>(h, h->vecT, h->cp, h->ri, h->rv, h->n, h->z, h->xi, nullptr, h->s, h->v);
+    k_csr_tiles<1><<<std::min(h->ntilesT, h->tile_grid), TG, sizeof(TileSmem), h->stream>>>(
+        h->cp, h->ri, h->rv, h->tilesT, h->ntilesT, h->z, h->xi, nullptr, h->s, h->v, h->st,
+        h->trace, h->bpart);
   }
 }
 
@@ -319,8 +355,9 @@ void launch_passN(rgdbek_ctx* h) {
     k_dense_reduceN<<<nblocks(h->m_loc, NT, MAXBLK), NT, 0, h->stream>>>(
         h->npart, h->nQ, (int)h->m_loc, h->b, h->w, h->ax, h->st, h->trace, h->bpart);
   } else {
-    launch_csr_vec<0>(h, h->vecN, h->rp, h->ci, h->cv, h->m_loc, h->zeta, h->x, h->b, h->w,
-                      h->ax);
+    k_csr_tiles<0><<<std::min(h->ntilesN, h->tile_grid), TG, sizeof(TileSmem), h->stream>>>(
+        h->rp, h->ci, h->cv, h->tilesN, h->ntilesN, h->zeta, h->x, h->b, h->w, h->ax, h->st,
+        h->trace, h->bpart);
   }
 }
 
@@ -502,7 +539,8 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
   }
   int nsm = 148, occ = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
-  h->p_dyn = std::max<size_t>(2 * ZCH * sizeof(double), (size_t)PN_RB * PN_QMAX * 2 * sizeof(double));
+  h->p_dyn = h->dense ? std::max<size_t>(2 * ZCH * sizeof(double), (size_t)PN_RB * PN_QMAX * 2 * sizeof(double))
+                     : (PT / TG) * sizeof(TileSmem);
   CK(h, cudaFuncSetAttribute(k_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->p_dyn));
   CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persistent, PT, h->p_dyn));
   if (occ < 1) return set_err(h, RGDBEK_E_CUDA, "persistent kernel cannot be resident (occupancy 0)");
@@ -547,6 +585,7 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
   a.r = h->r; a.xi = h->xi; a.keys_n = h->keys_n; a.keys_m = h->keys_m;
   a.part = ppart; a.bpart = h->bpart; a.hist = h->phist; a.cand = h->pcand; a.acc = h->pacc;
   a.ncand = h->pncand; a.st = h->st; a.tr = h->trace; a.bar = h->pbar;
+  a.tilesN = h->tilesN; a.tilesT = h->tilesT; a.ntilesN = h->ntilesN; a.ntilesT = h->ntilesT;
   if (const char* e = getenv("RGDBEK_PHASE_TIMING")) {
     if (atoi(e)) {
       TRY(dalloc(h, &h->ptime, 16));
@@ -963,6 +1002,20 @@ rgdbek_status rgdbek_create_csr(rgdbek_handle* out, int64_t m, int64_t n, int64_
   const double avg_c = (double)nnz_local / (double)h->n;
   h->vecN = pick_vec(avg_r);
   h->vecT = pick_vec(avg_c);
+  if ((s = build_tiles(h, h->rp, h->m_loc, &h->tilesN, &h->ntilesN)) != RGDBEK_OK) return create_fail(h, s);
+  if (h->cp == h->rp) {
+    h->tilesT = h->tilesN; h->ntilesT = h->ntilesN;
+  } else if ((s = build_tiles(h, h->cp, h->n, &h->tilesT, &h->ntilesT)) != RGDBEK_OK) {
+    return create_fail(h, s);
+  }
+  {
+    int nsm = 148, occ = 1;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
+    cudaFuncSetAttribute(k_csr_tiles<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem));
+    cudaFuncSetAttribute(k_csr_tiles<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_tiles<0>, TG, sizeof(TileSmem));
+    h->tile_grid = std::max(1, std::min(MAXBLK, nsm * std::max(occ, 1)));
+  }
   if ((s = finish_create(h)) != RGDBEK_OK) return create_fail(h, s);
   *out = h;
   return RGDBEK_OK;
