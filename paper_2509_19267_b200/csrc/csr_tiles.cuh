@@ -34,13 +34,37 @@ __device__ __forceinline__ void group_bar(int id) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(TG) : "memory");
 }
 
+// Optional fused epilogue of pass T (persistent engine): column scores
+// eps_j = s_j^2 / gamma_j, Philox keys and the level-1 histogram, and the
+// V = ||v||^2 partial, computed as each column sum is produced (the ALU work of
+// the keys overlaps the pass's memory traffic, and s, v are not re-read).
+struct ColKeyEpi {
+  const double* gamma;
+  unsigned long long* keys;
+  unsigned int* hist;      // shared-memory level-1 histogram of this CTA
+  long long k;
+  unsigned long long seed;
+  int pending;
+};
+
+__device__ __forceinline__ void colkey_epilogue(const ColKeyEpi* ep, int j, double sj, double vj,
+                                                double& Vp) {
+  if (ep->pending) Vp += vj * vj;
+  const double g = ep->gamma[j];
+  const double eps = g > 0.0 ? __ddiv_rn(__dmul_rn(sj, sj), g) : 0.0;
+  const unsigned long long key = make_key(eps, (unsigned long long)j, ep->k, 0u, ep->seed);
+  ep->keys[j] = key;
+  atomicAdd(&ep->hist[key >> L1_SHIFT], 1u);
+}
+
 __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm,
                           const long long* __restrict__ ptr, const int* __restrict__ idx,
                           const double* __restrict__ val, const int* __restrict__ tiles,
                           int ntiles, const double* __restrict__ in1,
                           const double* __restrict__ in2, int use2,
                           const double* __restrict__ b, double* __restrict__ o1,
-                          double* __restrict__ o2, double& Wp, double& Yp) {
+                          double* __restrict__ o2, double& Wp, double& Yp,
+                          const ColKeyEpi* ep = nullptr) {
   for (int t = gid; t < ntiles; t += ngroups) {
     const int r0 = tiles[t], r1 = tiles[t + 1];
     const int nr = r1 - r0;
@@ -69,17 +93,39 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
           Wp += s1 * s1;
           Yp += y * y;
         }
+        if (ep) colkey_epilogue(ep, r0, s1, s2, Wp);
       }
       group_bar(bar_id);
       continue;
     }
     const int nz = (int)(p1 - p0);
-#pragma unroll 4
-    for (int q = lt; q < nz; q += TG) {
-      const double a = ld_stream(val + p0 + q);
-      const int c = __ldg(idx + p0 + q);
-      sm->p1[q] = a * __ldg(in1 + c);
-      sm->p2[q] = use2 ? a * __ldg(in2 + c) : 0.0;
+    // sub-rounds of SUB entries per thread, each in two phases (all values /
+    // indices first, then all gathers), so SUB independent chains are in flight
+    constexpr int SUB = 4;
+    for (int e0 = 0; e0 < TILE_NNZ / TG; e0 += SUB) {
+      double av[SUB], g1[SUB], g2[SUB];
+      int ci[SUB];
+#pragma unroll
+      for (int e = 0; e < SUB; ++e) {
+        const int q = lt + (e0 + e) * TG;
+        av[e] = 0.0; ci[e] = 0;
+        if (q < nz) { av[e] = ld_stream(val + p0 + q); ci[e] = __ldg(idx + p0 + q); }
+      }
+#pragma unroll
+      for (int e = 0; e < SUB; ++e) {
+        const int q = lt + (e0 + e) * TG;
+        g1[e] = 0.0; g2[e] = 0.0;
+        if (q < nz) {
+          g1[e] = __ldg(in1 + ci[e]);
+          if (use2) g2[e] = __ldg(in2 + ci[e]);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < SUB; ++e) {
+        const int q = lt + (e0 + e) * TG;
+        if (q < nz) { sm->p1[q] = av[e] * g1[e]; sm->p2[q] = av[e] * g2[e]; }
+      }
+      if (lt + (e0 + SUB) * TG >= nz) break;
     }
     group_bar(bar_id);
     for (int r = lt; r < nr; r += TG) {
@@ -93,6 +139,7 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
         Wp += s1 * s1;
         Yp += y * y;
       }
+      if (ep) colkey_epilogue(ep, r0 + r, s1, s2, Wp);
     }
     group_bar(bar_id);
   }

@@ -654,24 +654,18 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
 
   for (;;) {
     // ===== P1: pass T  (s_k = A^T z_k, v_{k-1} = A^T xi_{k-1}) =====
-    double dummyW = 0.0, dummyY = 0.0;
-    if (a.dense) {
-      p_dense_passT(a, pending, dyn);
-    } else {
-      const int g = threadIdx.x / TG;
-      csr_tiles(blockIdx.x * (PT / TG) + g, G * (PT / TG), threadIdx.x % TG, 1 + g,
-                reinterpret_cast<TileSmem*>(dyn) + g, a.cp, a.ri, a.rv, a.tilesT, a.ntilesT,
-                a.z, a.xi, pending, nullptr, a.s, a.v, dummyW, dummyY);
-    }
-    grid_sync(a.bar);
-    PH(1);
-    p_zero_side(a, 1);                          // m-side buffers: consumed in P9..P12
-
-    // ===== P2: s, v; V; column scores and keys; level-1 histogram =====
-    for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
-    __syncthreads();
+    // Sparse: the column scores, keys, level-1 histogram and V partial are fused
+    // into the tile epilogue, so the separate P2 phase (and its barrier) vanishes.
     double Vp = 0.0;
     if (a.dense) {
+      p_dense_passT(a, pending, dyn);
+      grid_sync(a.bar);
+      PH(1);
+      p_zero_side(a, 1);                        // m-side buffers: consumed in P9..P12
+
+      // ===== P2 (dense): s, v = sum of the CTA partials; V; keys; level-1 histogram =====
+      for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
+      __syncthreads();
       const int lane = threadIdx.x & 31;
       const int gw = (blockIdx.x * PT + threadIdx.x) >> 5, nw = (G * PT) >> 5;
       for (int j = gw; j < n; j += nw) {
@@ -694,25 +688,33 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
           atomicAdd(&h[key >> L1_SHIFT], 1u);
         }
       }
-    } else {
-      for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) {
-        const double sj = a.s[j];
-        if (pending) { const double vj = a.v[j]; Vp += vj * vj; }
-        const double g = a.gamma[j];
-        const double eps = g > 0.0 ? __ddiv_rn(__dmul_rn(sj, sj), g) : 0.0;
-        const unsigned long long key = make_key(eps, (unsigned long long)j, k, 0u, seed);
-        a.keys_n[j] = key;
-        atomicAdd(&h[key >> L1_SHIFT], 1u);
+      __syncthreads();
+      flush_hist<PT>(h, hn, NBINS);
+      {
+        const double vb = pblock_sum(Vp, sh);
+        if (threadIdx.x == 0) bp[SL_V * G + blockIdx.x] = vb;
       }
+      grid_sync(a.bar);
+      PH(2);
+    } else {
+      for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
+      __syncthreads();
+      double dummyY = 0.0;
+      const ColKeyEpi ep{a.gamma, a.keys_n, h, k, seed, pending};
+      const int g = threadIdx.x / TG;
+      csr_tiles(blockIdx.x * (PT / TG) + g, G * (PT / TG), threadIdx.x % TG, 1 + g,
+                reinterpret_cast<TileSmem*>(dyn) + g, a.cp, a.ri, a.rv, a.tilesT, a.ntilesT,
+                a.z, a.xi, pending, nullptr, a.s, a.v, Vp, dummyY, &ep);
+      __syncthreads();
+      flush_hist<PT>(h, hn, NBINS);
+      {
+        const double vb = pblock_sum(Vp, sh);
+        if (threadIdx.x == 0) bp[SL_V * G + blockIdx.x] = vb;
+      }
+      grid_sync(a.bar);
+      PH(1);
+      p_zero_side(a, 1);                        // m-side buffers: consumed in P9..P12
     }
-    __syncthreads();
-    flush_hist<PT>(h, hn, NBINS);
-    {
-      const double vb = pblock_sum(Vp, sh);
-      if (threadIdx.x == 0) bp[SL_V * G + blockIdx.x] = vb;
-    }
-    grid_sync(a.bar);
-    PH(2);
 
     // ===== P3: V, alpha_x; level-1 bucket (U); level-2 scan =====
     const double V = slot_sum(bp, SL_V, sh);
