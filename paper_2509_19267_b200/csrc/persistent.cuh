@@ -22,7 +22,7 @@ constexpr int PW = PT / 32;
 constexpr int ZCH = 1024;                 // rows of z / xi staged per chunk (pass T)
 constexpr int PN_RB = 256;                // max rows per batch (dense pass N)
 constexpr int PN_QMAX = 8;                // max column chunks per row (dense pass N)
-constexpr int LOCAL_SEL_MAX = 16384;      // selections over <= this many keys run CTA-locally
+constexpr int LOCAL_SEL_MAX = 32768;      // selections over <= this many keys run CTA-locally
 
 struct GridBar {
   unsigned int count;
@@ -83,12 +83,16 @@ __device__ __forceinline__ void fence_acq_rel_gpu() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
-__device__ __forceinline__ void grid_sync(GridBar* gb) {
+// gen: thread 0's copy of the barrier generation (read once at kernel start).
+// The ticket RMWs form a release sequence on `count`; the last arriver
+// (acquire) publishes the next generation with a release store; waiters spin
+// on an acquire load (which also invalidates the SM's L1, so read-only-path
+// loads of vectors rewritten in earlier phases see the new values).
+__device__ __forceinline__ void grid_sync(GridBar* gb, unsigned int& gen) {
   __syncthreads();
   if (gridDim.x == 1) return;
   if (threadIdx.x == 0) {
-    const unsigned int g = ld_acquire_u32(&gb->gen);
-    fence_acq_rel_gpu();                    // this CTA's writes (ordered by bar.sync) first
+    const unsigned int g = gen++;
     const unsigned int t = atom_add_acqrel_u32(&gb->count, 1u);
     if (t == gridDim.x - 1) {
       gb->count = 0u;                       // ordered before the release below
@@ -96,10 +100,6 @@ __device__ __forceinline__ void grid_sync(GridBar* gb) {
     } else {
       while (ld_acquire_u32(&gb->gen) == g) { }
     }
-    // gpu-scope fence: also invalidates this SM's L1 (CCTL.IVALL), so the
-    // read-only-path loads (__ldg) of vectors rewritten in earlier phases
-    // (zeta, x, z, xi) see the new values.
-    fence_acq_rel_gpu();
   }
   __syncthreads();
 }
@@ -644,6 +644,8 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
   Cand* cn = a.cand;
   Cand* cm = a.cand + CAND_CAP;
   unsigned long long t_last = 0;
+  unsigned int bgen = 0;
+  if (threadIdx.x == 0) bgen = ld_acquire_u32(&a.bar->gen);
 #define PH(i)                                                        \
   if (a.ptime && lead) {                                             \
     const unsigned long long t_ = gtimer();                          \
@@ -659,42 +661,71 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     double Vp = 0.0;
     if (a.dense) {
       p_dense_passT(a, pending, dyn);
-      grid_sync(a.bar);
+      grid_sync(a.bar, bgen);
       PH(1);
       p_zero_side(a, 1);                        // m-side buffers: consumed in P9..P12
 
       // ===== P2 (dense): s, v = sum of the CTA partials; V; keys; level-1 histogram =====
       for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
       __syncthreads();
-      const int lane = threadIdx.x & 31;
-      const int gw = (blockIdx.x * PT + threadIdx.x) >> 5, nw = (G * PT) >> 5;
-      for (int j = gw; j < n; j += nw) {
-        double sj = 0.0, vj = 0.0;
-        for (int p = lane; p < G; p += 32) {
-          const double* q = a.part + (long long)p * 2 * n + j;
-          sj += __ldcg(q);
-          if (pending) vj += __ldcg(q + n);
-        }
-        sj = warp_sum(sj);
-        vj = warp_sum(vj);
-        if (lane == 0) {
-          a.s[j] = sj;
-          a.v[j] = vj;
-          if (pending) Vp += vj * vj;
-          const double g = a.gamma[j];
-          const double eps = g > 0.0 ? __ddiv_rn(__dmul_rn(sj, sj), g) : 0.0;
-          const unsigned long long key = make_key(eps, (unsigned long long)j, k, 0u, seed);
-          a.keys_n[j] = key;
-          atomicAdd(&h[key >> L1_SHIFT], 1u);
+      // CTA b owns columns [c0, c1); thread (c = tid % 64, g = tid / 64) sums the
+      // partials p = g, g + 16, ... of column c0 + chunk + c (coalesced across c),
+      // then the 16 group sums are added in group order (deterministic) and one
+      // thread per column makes its key — all columns of a CTA in parallel.
+      {
+        constexpr int CW = 64, NG = PT / CW;
+        double* red = dyn;                        // [2][NG][CW]
+        const int cpb = (n + G - 1) / G;
+        const int c0 = min(n, blockIdx.x * cpb), c1 = min(n, c0 + cpb);
+        const int cl = threadIdx.x % CW, g = threadIdx.x / CW;
+        for (int cb = c0; cb < c1; cb += CW) {
+          const int j = cb + cl;
+          double sj = 0.0, vj = 0.0;
+          if (j < c1) {
+            double ps[10], pv[10];
+#pragma unroll
+            for (int t = 0; t < 10; ++t) {
+              const int p = g + NG * t;
+              const double* q = a.part + (long long)p * 2 * n + j;
+              ps[t] = p < G ? __ldcg(q) : 0.0;
+              pv[t] = (p < G && pending) ? __ldcg(q + n) : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < 10; ++t) { sj += ps[t]; vj += pv[t]; }
+            for (int p = g + NG * 10; p < G; p += NG) {       // G > 160 (not on B200)
+              const double* q = a.part + (long long)p * 2 * n + j;
+              sj += __ldcg(q);
+              if (pending) vj += __ldcg(q + n);
+            }
+          }
+          red[g * CW + cl] = sj;
+          red[(NG + g) * CW + cl] = vj;
+          __syncthreads();
+          if (g == 0 && j < c1) {
+            double ts = 0.0, tv = 0.0;
+#pragma unroll
+            for (int q = 0; q < NG; ++q) { ts += red[q * CW + cl]; tv += red[(NG + q) * CW + cl]; }
+            a.s[j] = ts;
+            a.v[j] = tv;
+            if (pending) Vp += tv * tv;
+            const double gm = a.gamma[j];
+            const double eps = gm > 0.0 ? __ddiv_rn(__dmul_rn(ts, ts), gm) : 0.0;
+            const unsigned long long key = make_key(eps, (unsigned long long)j, k, 0u, seed);
+            a.keys_n[j] = key;
+            atomicAdd(&h[key >> L1_SHIFT], 1u);
+          }
+          __syncthreads();
         }
       }
       __syncthreads();
+      PH(11);
       flush_hist<PT>(h, hn, NBINS);
       {
         const double vb = pblock_sum(Vp, sh);
         if (threadIdx.x == 0) bp[SL_V * G + blockIdx.x] = vb;
       }
-      grid_sync(a.bar);
+      PH(12);
+      grid_sync(a.bar, bgen);
       PH(2);
     } else {
       for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
@@ -711,7 +742,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
         const double vb = pblock_sum(Vp, sh);
         if (threadIdx.x == 0) bp[SL_V * G + blockIdx.x] = vb;
       }
-      grid_sync(a.bar);
+      grid_sync(a.bar, bgen);
       PH(1);
       p_zero_side(a, 1);                        // m-side buffers: consumed in P9..P12
     }
@@ -728,12 +759,12 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       p_sel_local(&ps, a.keys_n, n, 0, h, sh_u, sh_l);
     } else {
       p_sel_scan<2>(&ps, a.keys_n, n, 0, hn + NBINS, cn, a.ncand, h);
-      grid_sync(a.bar);
+      grid_sync(a.bar, bgen);
       PH(3);
       // ===== P4: level-2 bucket; level-3 scan + candidates =====
       p_sel_level2(&ps, hn + NBINS, sh_u, sh_l);
       p_sel_scan<3>(&ps, a.keys_n, n, 0, hn + 2 * NBINS, cn, a.ncand, h);
-      grid_sync(a.bar);
+      grid_sync(a.bar, bgen);
       PH(4);
       // ===== P5: exact threshold =====
       p_sel_level3(&ps, hn + 2 * NBINS, cn, a.ncand, a.keys_n, n, 0, h, sh_u, sh_l);
@@ -763,7 +794,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       if (threadIdx.x == 0) { bp[SL_Z * G + blockIdx.x] = zb; bp[SL_R * G + blockIdx.x] = rb; }
     }
     pending = 0;
-    grid_sync(a.bar);
+    grid_sync(a.bar, bgen);
     PH(5);
 
     // ===== P6: Z, |U|; pass N (w = A zeta, A x_k) with W / ||b - Ax||^2 partials =====
@@ -789,7 +820,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       const double yb = pblock_sum(Yp, sh);
       if (threadIdx.x == 0) { bp[SL_W * G + blockIdx.x] = wb; bp[SL_Y * G + blockIdx.x] = yb; }
     }
-    grid_sync(a.bar);
+    grid_sync(a.bar, bgen);
     PH(6);
 
     // ===== P8: stop test on x_k; z_{k+1}, r, row scores and keys, level-1 histogram =====
@@ -840,7 +871,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     __syncthreads();
     flush_hist<PT>(h, hm, NBINS);
     p_zero_side(a, 0);                          // n-side buffers: consumed in P3..P6
-    grid_sync(a.bar);
+    grid_sync(a.bar, bgen);
     PH(7);
 
     // ===== P9: level-1 bucket (J); level-2 scan =====
@@ -849,12 +880,12 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       p_sel_local(&ps, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
     } else {
       p_sel_scan<2>(&ps, a.keys_m, m_loc, a.row0, hm + NBINS, cm, a.ncand + 1, h);
-      grid_sync(a.bar);
+      grid_sync(a.bar, bgen);
       PH(8);
       // ===== P10: level-2 bucket; level-3 scan + candidates =====
       p_sel_level2(&ps, hm + NBINS, sh_u, sh_l);
       p_sel_scan<3>(&ps, a.keys_m, m_loc, a.row0, hm + 2 * NBINS, cm, a.ncand + 1, h);
-      grid_sync(a.bar);
+      grid_sync(a.bar, bgen);
       PH(9);
       // ===== P11: exact threshold =====
       p_sel_level3(&ps, hm + 2 * NBINS, cm, a.ncand + 1, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
@@ -880,7 +911,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       const double xb = pblock_sum(Xp, sh);
       if (threadIdx.x == 0) bp[SL_X * G + blockIdx.x] = xb;
     }
-    grid_sync(a.bar);
+    grid_sync(a.bar, bgen);
     PH(10);
 
     // ===== P12: X, |J|; bookkeeping; k++ =====

@@ -14,7 +14,7 @@ sys.path.insert(0, ROOT)
 
 PHASES = {1: "passT", 2: "s_v_colkeys_L1", 3: "colsel_L2", 4: "colsel_L3", 5: "mask_x_update",
           6: "passN", 7: "stop_z_rowkeys_L1", 8: "rowsel_L2", 9: "rowsel_L3", 10: "row_mask",
-          0: "bookkeeping"}
+          0: "bookkeeping", 11: "dense_P2_columns", 12: "dense_P2_flush_sum"}
 
 
 def main():
