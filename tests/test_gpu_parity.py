@@ -308,3 +308,18 @@ def test_sharded_code_path_world1_nccl(name):
         destroy_nccl_comm(comm)
     finally:
         dist.destroy_process_group()
+
+
+def test_time_to_tolerance_c5s_scaled_twin():
+    """C5s (50000x5000, 1e6 nnz, the oracle-feasible twin of C5): iterations to
+    ||x - x*||/||x*|| <= 1e-6 within 2 % of the oracle's (~5.7k iterations)."""
+    from oracle import STOP_REL_ERR
+    from workloads import by_name
+    w = by_name("C5s")
+    s = _solver(w, stop="rel_err")
+    s.set_reference(w.xstar)
+    res = s.solve(1e-6, 100000, 0)
+    o = _oracle(w)
+    out, iters, _, _ = o.solve(1e-6, 100000, 0, stop=STOP_REL_ERR, xstar=w.xstar)
+    assert abs(res["iters"] - iters) <= int(0.02 * iters), (res["iters"], iters)
+    s.close()
