@@ -148,6 +148,15 @@ rgdbek_status rgdbek_solve(rgdbek_handle h, double tol, int64_t max_iter, uint64
                            rgdbek_result* result);
 
 rgdbek_status rgdbek_set_stop(rgdbek_handle h, int32_t stop);
+
+/* Update mode.  mode 0 (default): the pseudoinverse-free block updates
+ * of BASELINE.json's north_star.  mode 1: Algorithm 1's exact projections
+ *   z_{k+1} = z_k - A_U A_U^+ z_k,  x_{k+1} = x_k + (A^J)^+ (b^J - z^J - A^J x_k),
+ * realised by inner CGLS iterations (minimum-norm, from 0) on the masked operators
+ * — the Krylov solvers equivalent to the paper's LSQR — each stopped when its
+ * residual has dropped by inner_tol (relative) or after inner_max iterations.  mode 1 needs the
+ * single-GPU persistent engine (RGDBEK_E_STATE otherwise). */
+rgdbek_status rgdbek_set_mode(rgdbek_handle h, int32_t mode, double inner_tol, int32_t inner_max);
 rgdbek_status rgdbek_set_reference(rgdbek_handle h, const double* xstar /* n values */);
 
 rgdbek_status rgdbek_get_x(rgdbek_handle h, double* out_n);

@@ -25,6 +25,10 @@ What it computes (PAPER.md = /root/reference/PAPER.md, cited as P:<line>):
     eta^T r = ||xi||^2 = X, in place of the pseudoinverse of P:122).
   - Stop test on RSE = ||A x - b||^2 / ||b||^2 or on
     ||x - x*|| / ||x*|| (BASELINE.json metric), after each full iteration.
+* update="exact": Algorithm 1's own updates, z_{k+1} =
+  z_k - A_U A_U^+ z_k and x_{k+1} = x_k + (A^J)^+ r^J, written
+  out with numpy's minimum-norm least-squares solver (lstsq) on the extracted
+  submatrices.
 * No blocking, fusion or reordering: every product is one library matvec
   (numpy BLAS for dense A, scipy.sparse for CSR A), every selection one sort.
 
@@ -144,7 +148,10 @@ class IterRecord:
 class Oracle:
     """State (x_k, z_k, k) of Algorithm 1 and its plain iteration."""
 
-    def __init__(self, A, b, eta=0.5):
+    def __init__(self, A, b, eta=0.5, update="pinv_free"):
+        if update not in ("pinv_free", "exact"):
+            raise ValueError("update must be 'pinv_free' or 'exact'")
+        self.update = update
         self.A = A
         self.b = np.asarray(b, dtype=np.float64)
         self.m, self.n = A.shape
@@ -184,7 +191,14 @@ class Oracle:
         Z = float(s[U] @ s[U])
         w = A @ zeta
         W = float(w @ w)
-        if kp > 0 and W > 0:                               # reading R7
+        if self.update == "exact":
+            # z_{k+1} = z_k - A_U A_U^+ z_k: the orthogonal projection of z_k
+            # onto range(A_U)^perp, via the minimum-norm least-squares solution
+            if kp > 0:
+                AU = A[:, U] if isinstance(A, np.ndarray) else A[:, U].toarray()
+                y = np.linalg.lstsq(AU, z, rcond=None)[0]
+                self.z = z - AU @ y
+        elif kp > 0 and W > 0:                             # reading R7
             self.z = z - (Z / W) * w
         return kp, U, Z, W
 
@@ -201,7 +215,12 @@ class Oracle:
         X = float(r[J] @ r[J])
         v = A.T @ xi
         V = float(v @ v)
-        if kpp > 0 and V > 0:
+        if self.update == "exact":
+            # x_{k+1} = x_k + (A^J)^+ (b^J - z^J_{k+1} - A^J x_k), minimum-norm LS
+            if kpp > 0:
+                AJ = A[J, :] if isinstance(A, np.ndarray) else A[J, :].toarray()
+                self.x = self.x + np.linalg.lstsq(AJ, r[J], rcond=None)[0]
+        elif kpp > 0 and V > 0:
             self.x = self.x + (X / V) * v
         return kpp, J, X, V
 

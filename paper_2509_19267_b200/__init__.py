@@ -144,6 +144,11 @@ class Solver:
         """Per-phase device ns of the persistent engine (RGDBEK_PHASE_TIMING=1), else []."""
         return N.rgdbek_phase_times(self._h)
 
+    def set_mode(self, mode, inner_tol=1e-12, inner_max=50):
+        """'pinv_free' (default) or 'exact' (Alg. 1's projections via inner CGLS)."""
+        m = {"pinv_free": 0, "exact": 1}[mode] if isinstance(mode, str) else int(mode)
+        N.rgdbek_set_mode(self._h, m, inner_tol, inner_max)
+
     def engine_info(self):
         """(engine, ctas): engine 0 = persistent kernel, 1 = CUDA-graph engine."""
         return N.rgdbek_engine_info(self._h)

@@ -8,7 +8,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librgdbek.so")
 SOURCES = ["runtime.cu"]
-HEADERS = ["common.cuh", "select.cuh", "kernels.cuh", "persistent.cuh", "csr_tiles.cuh"]
+HEADERS = ["common.cuh", "select.cuh", "kernels.cuh", "persistent.cuh", "csr_tiles.cuh", "exact.cuh"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

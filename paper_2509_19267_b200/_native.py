@@ -22,7 +22,7 @@ EXPORTED = [
     "rgdbek_reset", "rgdbek_step", "rgdbek_solve", "rgdbek_set_stop", "rgdbek_set_reference",
     "rgdbek_get_x", "rgdbek_get_z", "rgdbek_get_blocks", "rgdbek_get_trace", "rgdbek_set_state",
     "rgdbek_launch_kernel", "rgdbek_launches_per_iteration", "rgdbek_stream",
-    "rgdbek_phase_times", "rgdbek_engine_info",
+    "rgdbek_phase_times", "rgdbek_engine_info", "rgdbek_set_mode",
     "rgdbek_nccl_unique_id", "rgdbek_nccl_comm_init", "rgdbek_nccl_comm_destroy",
     "rgdbek_last_error", "rgdbek_destroy",
 ]
@@ -93,6 +93,7 @@ def load(path=None):
         "rgdbek_phase_times": (C.c_int, [H, C.POINTER(C.c_double), C.c_int32,
                                          C.POINTER(C.c_int32)]),
         "rgdbek_engine_info": (C.c_int, [H, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+        "rgdbek_set_mode": (C.c_int, [H, C.c_int32, C.c_double, C.c_int32]),
         "rgdbek_nccl_unique_id": (C.c_int, [P]),
         "rgdbek_nccl_comm_init": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, P,
                                             C.c_int32]),
@@ -213,6 +214,10 @@ def rgdbek_phase_times(h):
     cnt = C.c_int32()
     check(load().rgdbek_phase_times(h, buf, 16, C.byref(cnt)), h)
     return [buf[i] for i in range(cnt.value)]
+
+
+def rgdbek_set_mode(h, mode, inner_tol=1e-12, inner_max=50):
+    check(load().rgdbek_set_mode(h, int(mode), float(inner_tol), int(inner_max)), h)
 
 
 def rgdbek_engine_info(h):

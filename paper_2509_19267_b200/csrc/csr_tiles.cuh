@@ -64,7 +64,7 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
                           const double* __restrict__ in2, int use2,
                           const double* __restrict__ b, double* __restrict__ o1,
                           double* __restrict__ o2, double& Wp, double& Yp,
-                          const ColKeyEpi* ep = nullptr) {
+                          const ColKeyEpi* ep = nullptr, int acc1 = 0) {
   for (int t = gid; t < ntiles; t += ngroups) {
     const int r0 = tiles[t], r1 = tiles[t + 1];
     const int nr = r1 - r0;
@@ -94,6 +94,7 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
           Yp += y * y;
         }
         if (ep) colkey_epilogue(ep, r0, s1, s2, Wp);
+        if (acc1) Wp += s1 * s1;
       }
       group_bar(bar_id);
       continue;
@@ -140,6 +141,7 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
         Yp += y * y;
       }
       if (ep) colkey_epilogue(ep, r0 + r, s1, s2, Wp);
+      if (acc1) Wp += s1 * s1;
     }
     group_bar(bar_id);
   }

@@ -432,7 +432,10 @@ __device__ __forceinline__ bool p_selected(const PSel* ps, unsigned long long ke
 // Dense pass T for this CTA's contiguous row range, all columns (column tiles
 // of 2*PT): part[cta][0][j] = sum_i A_ij z_i, part[cta][1][j] = sum_i A_ij xi_i.
 // ---------------------------------------------------------------------------
-__device__ void p_dense_passT(const PArgs& a, int pending, double* zs) {
+__device__ void p_dense_passT(const PArgs& a, int pending, double* zs,
+                              const double* in1 = nullptr, const double* in2 = nullptr) {
+  if (!in1) in1 = a.z;
+  if (!in2) in2 = a.xi;
   const int G = gridDim.x, bb = blockIdx.x;
   const int rb = (int)((long long)a.m_loc * bb / G), re = (int)((long long)a.m_loc * (bb + 1) / G);
   const int ntiles = (a.n + 2 * PT - 1) / (2 * PT);
@@ -444,8 +447,8 @@ __device__ void p_dense_passT(const PArgs& a, int pending, double* zs) {
       const int rows = min(ZCH, re - rc);
       __syncthreads();
       for (int i = threadIdx.x; i < rows; i += PT) {
-        zs[i] = a.z[rc + i];
-        zs[ZCH + i] = pending ? a.xi[rc + i] : 0.0;
+        zs[i] = in1[rc + i];
+        zs[ZCH + i] = pending ? in2[rc + i] : 0.0;
       }
       __syncthreads();
       const double* p = a.A + (long long)rc * a.lda + c;
@@ -482,7 +485,15 @@ __device__ void p_dense_passT(const PArgs& a, int pending, double* zs) {
 // (1 row) x (column chunk of CH), partials in smem, summed in chunk order.
 // Returns this thread's contributions to W and ||b - Ax||^2.
 // ---------------------------------------------------------------------------
-__device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp) {
+__device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp,
+                              const double* in1 = nullptr, const double* in2 = nullptr,
+                              double* out1 = nullptr, double* out2 = nullptr,
+                              const double* bvec = nullptr, bool use_b = true) {
+  if (!in1) in1 = a.zeta;
+  if (!in2) in2 = a.x;
+  if (!out1) out1 = a.w;
+  if (!out2) out2 = a.ax;
+  if (!bvec && use_b) bvec = a.b;
   const int G = gridDim.x, bb = blockIdx.x;
   const int rb = (int)((long long)a.m_loc * bb / G), re = (int)((long long)a.m_loc * (bb + 1) / G);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -503,8 +514,8 @@ __device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp
       double w0 = 0.0, x0 = 0.0, w1 = 0.0, x1 = 0.0;
 #pragma unroll 4
       for (int c = c0 + lane * 2; c < c1e; c += 64) {
-        const double2 zc = __ldg(reinterpret_cast<const double2*>(a.zeta + c));
-        const double2 xc = __ldg(reinterpret_cast<const double2*>(a.x + c));
+        const double2 zc = __ldg(reinterpret_cast<const double2*>(in1 + c));
+        const double2 xc = __ldg(reinterpret_cast<const double2*>(in2 + c));
         const double2 v0 = ld_stream2(a0 + c);
         const double2 v1 = two ? ld_stream2(a1 + c) : make_double2(0.0, 0.0);
         w0 = fma(v0.x, zc.x, w0); w0 = fma(v0.y, zc.y, w0);
@@ -514,12 +525,12 @@ __device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp
       }
       if (c1e < c1 && lane == 0) {
         const double v0 = ld_stream(a0 + c1e);
-        w0 = fma(v0, a.zeta[c1e], w0);
-        x0 = fma(v0, a.x[c1e], x0);
+        w0 = fma(v0, in1[c1e], w0);
+        x0 = fma(v0, in2[c1e], x0);
         if (two) {
           const double v1 = ld_stream(a1 + c1e);
-          w1 = fma(v1, a.zeta[c1e], w1);
-          x1 = fma(v1, a.x[c1e], x1);
+          w1 = fma(v1, in1[c1e], w1);
+          x1 = fma(v1, in2[c1e], x1);
         }
       }
       w0 = warp_sum(w0); x0 = warp_sum(x0);
@@ -534,11 +545,15 @@ __device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp
       const int rr = threadIdx.x, i = r0 + rr;
       double tw = 0.0, tx = 0.0;
       for (int q = 0; q < Q; ++q) { tw += np[(rr * PN_QMAX + q) * 2]; tx += np[(rr * PN_QMAX + q) * 2 + 1]; }
-      a.w[i] = tw;
-      a.ax[i] = tx;
-      const double y = a.b[i] - tx;
+      out1[i] = tw;
+      out2[i] = tx;
       Wp += tw * tw;
-      Yp += y * y;
+      if (bvec) {
+        const double y = bvec[i] - tx;
+        Yp += y * y;
+      } else {
+        Yp += tx * tx;
+      }
     }
     __syncthreads();
   }

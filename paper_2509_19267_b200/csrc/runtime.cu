@@ -19,7 +19,7 @@
 #include <string>
 #include <vector>
 
-#include "persistent.cuh"
+#include "exact.cuh"
 
 using namespace rg;
 
@@ -83,6 +83,8 @@ struct rgdbek_ctx {
   Cand* surv_all = nullptr;             // [nranks][SURV_CAP + 1]
   int nccl_fail = 0;
   unsigned long long* ptime = nullptr;  // persistent: per-phase ns (RGDBEK_PHASE_TIMING=1)
+  int mode = 0;                         // 0 = pseudoinverse-free, 1 = exact projection
+  EArgs eargs{};
   // vectors
   double *b = nullptr, *rho = nullptr, *gamma = nullptr;
   double *x = nullptr, *s = nullptr, *v = nullptr, *zeta = nullptr, *xstar = nullptr;
@@ -542,6 +544,7 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
   h->p_dyn = h->dense ? std::max<size_t>(2 * ZCH * sizeof(double), (size_t)PN_RB * PN_QMAX * 2 * sizeof(double))
                      : (PT / TG) * sizeof(TileSmem);
   CK(h, cudaFuncSetAttribute(k_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->p_dyn));
+  CK(h, cudaFuncSetAttribute(k_persistent_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->p_dyn));
   CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persistent, PT, h->p_dyn));
   if (occ < 1) return set_err(h, RGDBEK_E_CUDA, "persistent kernel cannot be resident (occupancy 0)");
   // CTAs: about one per MB of per-iteration traffic, at most one per SM
@@ -597,6 +600,12 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
 }
 
 rgdbek_status launch_persistent(rgdbek_ctx* h) {
+  if (h->mode == 1) {
+    void* args[] = {(void*)&h->pargs, (void*)&h->eargs};
+    CK(h, cudaLaunchCooperativeKernel((const void*)k_persistent_exact, dim3(h->pG), dim3(PT), args,
+                                      h->p_dyn, h->stream));
+    return RGDBEK_OK;
+  }
   void* args[] = {(void*)&h->pargs};
   CK(h, cudaLaunchCooperativeKernel((const void*)k_persistent, dim3(h->pG), dim3(PT), args,
                                     h->p_dyn, h->stream));
@@ -1187,6 +1196,28 @@ rgdbek_status rgdbek_phase_times(rgdbek_handle h, double* out_ns, int32_t max_ph
   const int cnt = std::min(16, (int)max_phases);
   for (int i = 0; i < cnt; ++i) out_ns[i] = (double)t[i];
   *n_out = cnt;
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_set_mode(rgdbek_handle h, int32_t mode, double inner_tol, int32_t inner_max) {
+  TRY(ensure_usable(h));
+  if (mode < 0 || mode > 1) return set_err(h, RGDBEK_E_ARG, "unknown update mode %d", mode);
+  if (mode == 1) {
+    if (!(inner_tol > 0.0 && inner_tol < 1.0) || inner_max < 1)
+      return set_err(h, RGDBEK_E_ARG, "exact mode needs 0 < inner_tol < 1 and inner_max >= 1");
+    if (h->engine != 0 || h->dist)
+      return set_err(h, RGDBEK_E_STATE, "exact-projection mode runs on the single-GPU persistent engine");
+    int occ = 0;
+    CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persistent_exact, PT, h->p_dyn));
+    if (occ < 1) return set_err(h, RGDBEK_E_CUDA, "exact-mode kernel cannot be resident");
+    if (!h->eargs.px) {
+      TRY(dalloc(h, &h->eargs.px, h->n));
+      TRY(dalloc(h, &h->eargs.u, h->m_loc));
+    }
+    h->eargs.inner_tol = inner_tol;
+    h->eargs.inner_max = inner_max;
+  }
+  h->mode = mode;
   return RGDBEK_OK;
 }
 

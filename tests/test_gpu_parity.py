@@ -323,3 +323,42 @@ def test_time_to_tolerance_c5s_scaled_twin():
     out, iters, _, _ = o.solve(1e-6, 100000, 0, stop=STOP_REL_ERR, xstar=w.xstar)
     assert abs(res["iters"] - iters) <= int(0.02 * iters), (res["iters"], iters)
     s.close()
+
+
+@pytest.mark.parametrize("name,inner_max", [("C2s", 200), ("C2si", 200), ("C5t", 400), ("C3s", 2000)])
+def test_exact_projection_mode(name, inner_max):
+    """NEXT #1: Alg. 1's exact projections through inner CGLS on the
+    GPU vs numpy lstsq in the oracle: same blocks, x and z to 1e-8 (the inner
+    solves stop at a 1e-13 relative normal-equation residual)."""
+    from oracle import Oracle
+    from workloads import by_name
+    w = by_name(name)
+    s = _solver(w)
+    s.set_mode("exact", inner_tol=1e-13, inner_max=inner_max)
+    o = Oracle(w.A, w.b, w.eta, update="exact")
+    s.reset(5)
+    bn = np.linalg.norm(w.b)
+    for k in range(8):
+        rec = o.iterate(5)
+        s.step(1)
+        g = s.trace()[-1]
+        assert (g["kp"], g["hash_u"], g["kpp"], g["hash_j"]) == (rec.kp, rec.hash_u, rec.kpp, rec.hash_j), k
+        assert abs(g["Z"] - rec.Z) <= 1e-9 * rec.Z and abs(g["X"] - rec.X) <= 1e-8 * rec.X
+        assert np.linalg.norm(s.x() - o.x) <= 1e-8 * np.linalg.norm(o.x), k
+        assert np.linalg.norm(s.z() - o.z) <= 1e-8 * bn, k
+    s.close()
+
+
+def test_exact_mode_time_to_tolerance():
+    from oracle import Oracle, STOP_REL_ERR
+    from paper_2509_19267_b200 import RGDBEK_CONVERGED
+    from workloads import by_name
+    w = by_name("C2s")
+    s = _solver(w, stop="rel_err")
+    s.set_mode("exact", inner_tol=1e-13, inner_max=200)
+    s.set_reference(w.xstar)
+    res = s.solve(1e-6, 1000, 0)
+    o = Oracle(w.A, w.b, w.eta, update="exact")
+    out, iters, _, _ = o.solve(1e-6, 1000, 0, stop=STOP_REL_ERR, xstar=w.xstar)
+    assert res["outcome"] == RGDBEK_CONVERGED == out
+    assert abs(res["iters"] - iters) <= max(1, int(0.02 * iters)), (res["iters"], iters)
