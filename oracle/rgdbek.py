@@ -148,10 +148,12 @@ class IterRecord:
 class Oracle:
     """State (x_k, z_k, k) of Algorithm 1 and its plain iteration."""
 
-    def __init__(self, A, b, eta=0.5, update="pinv_free"):
-        if update not in ("pinv_free", "exact"):
-            raise ValueError("update must be 'pinv_free' or 'exact'")
+    def __init__(self, A, b, eta=0.5, update="pinv_free", inner_tol=1e-13, inner_max=50):
+        if update not in ("pinv_free", "exact", "exact_lstsq"):
+            raise ValueError("update must be 'pinv_free', 'exact' or 'exact_lstsq'")
         self.update = update
+        self.inner_tol = float(inner_tol)
+        self.inner_max = int(inner_max)
         self.A = A
         self.b = np.asarray(b, dtype=np.float64)
         self.m, self.n = A.shape
@@ -191,13 +193,40 @@ class Oracle:
         Z = float(s[U] @ s[U])
         w = A @ zeta
         W = float(w @ w)
-        if self.update == "exact":
+        if self.update == "exact_lstsq":
             # z_{k+1} = z_k - A_U A_U^+ z_k: the orthogonal projection of z_k
             # onto range(A_U)^perp, via the minimum-norm least-squares solution
             if kp > 0:
                 AU = A[:, U] if isinstance(A, np.ndarray) else A[:, U].toarray()
                 y = np.linalg.lstsq(AU, z, rcond=None)[0]
                 self.z = z - AU @ y
+        elif self.update == "exact":
+            # the same projection by the paper's route, an inner Krylov solve of
+            # min ||A_U y - z_k|| (LSQR; here its equivalent CGLS, reading
+            # R1b), from y = 0; z holds its residual z_k - A_U y.  Stopping rule:
+            # ||A_U^T z||^2 <= inner_tol^2 Z, or inner_max iterations.
+            if kp > 0:
+                p, gam = zeta.copy(), Z
+                z = z.copy()
+                inU = np.zeros(self.n, dtype=bool)
+                inU[U] = True
+                for it in range(self.inner_max):
+                    if not gam > 0:
+                        break
+                    q = A @ p
+                    Wq = float(q @ q)
+                    if not Wq > 0:
+                        break
+                    z = z - (gam / Wq) * q
+                    if it + 1 == self.inner_max:
+                        break
+                    sp = A.T @ z
+                    gnew = float(sp[inU] @ sp[inU])
+                    if gnew <= self.inner_tol ** 2 * Z:
+                        break
+                    p = np.where(inU, sp + (gnew / gam) * p, 0.0)
+                    gam = gnew
+                self.z = z
         elif kp > 0 and W > 0:                             # reading R7
             self.z = z - (Z / W) * w
         return kp, U, Z, W
@@ -215,11 +244,41 @@ class Oracle:
         X = float(r[J] @ r[J])
         v = A.T @ xi
         V = float(v @ v)
-        if self.update == "exact":
+        if self.update == "exact_lstsq":
             # x_{k+1} = x_k + (A^J)^+ (b^J - z^J_{k+1} - A^J x_k), minimum-norm LS
             if kpp > 0:
                 AJ = A[J, :] if isinstance(A, np.ndarray) else A[J, :].toarray()
                 self.x = self.x + np.linalg.lstsq(AJ, r[J], rcond=None)[0]
+        elif self.update == "exact":
+            # inner CGLS on min ||A^J y - r^J|| from y = 0 (limit (A^J)^+ r^J); stopping
+            # rule ||A^J^T res||^2 <= inner_tol^2 ||A^J^T r^J||^2, or inner_max iterations
+            if kpp > 0 and X > 0:
+                inJ = np.zeros(self.m, dtype=bool)
+                inJ[J] = True
+                res = xi.copy()
+                t = A.T @ res
+                p = t.copy()
+                gam0 = gam = float(t @ t)
+                x = self.x.copy()
+                for it in range(self.inner_max):
+                    if not gam > 0:
+                        break
+                    u = A @ p
+                    Wq = float(u[inJ] @ u[inJ])
+                    if not Wq > 0:
+                        break
+                    al = gam / Wq
+                    x = x + al * p
+                    res = np.where(inJ, res - al * u, 0.0)
+                    if it + 1 == self.inner_max:
+                        break
+                    t = A.T @ res
+                    gnew = float(t @ t)
+                    if gnew <= self.inner_tol ** 2 * gam0:
+                        break
+                    p = t + (gnew / gam) * p
+                    gam = gnew
+                self.x = x
         elif kpp > 0 and V > 0:
             self.x = self.x + (X / V) * v
         return kpp, J, X, V

@@ -32,7 +32,7 @@ def _cgls(A, rhs, iters):
 @pytest.mark.parametrize("noise", [0.0, 0.2])
 def test_exact_z_step_is_orthogonal_projection(noise):
     w = dense_gaussian(120, 30, seed=3, noise=noise)
-    o = Oracle(w.A, w.b, 0.4, update="exact")
+    o = Oracle(w.A, w.b, 0.4, update="exact_lstsq")
     for _ in range(4):
         z_old = o.z.copy()
         kp, U, Z, W = o.column_step(seed=2)
@@ -51,7 +51,7 @@ def test_exact_z_step_is_orthogonal_projection(noise):
 def test_exact_x_step_min_norm_fat_block():
     # |J| < n: A^J has full row rank, the selected equations are solved exactly
     w = dense_gaussian(60, 40, seed=5)
-    o = Oracle(w.A, w.b, 0.3, update="exact")
+    o = Oracle(w.A, w.b, 0.3, update="exact_lstsq")
     o.column_step(seed=1)
     x0 = o.x.copy()
     r = w.b - o.z - w.A @ x0
@@ -69,7 +69,7 @@ def test_exact_x_step_min_norm_fat_block():
 def test_exact_x_step_least_squares_tall_block():
     # |J| > n: the correction is the least-squares solution, normal equations hold on J
     w = dense_gaussian(200, 20, seed=6, noise=0.3)
-    o = Oracle(w.A, w.b, 0.5, update="exact")
+    o = Oracle(w.A, w.b, 0.5, update="exact_lstsq")
     o.column_step(seed=4)
     x0 = o.x.copy()
     kpp, J, X, V = o.row_step(seed=4)
@@ -81,7 +81,7 @@ def test_exact_x_step_least_squares_tall_block():
 
 def test_exact_mode_limits_and_fewer_iterations():
     w = dense_gaussian(300, 60, seed=1, noise=0.1)
-    oe = Oracle(w.A, w.b, 0.5, update="exact")
+    oe = Oracle(w.A, w.b, 0.5, update="exact_lstsq")
     out, it_e, _, _ = oe.solve(1e-10, 2000, 3, stop=STOP_REL_ERR, xstar=w.xstar)
     assert out == OUTCOME_CONVERGED
     np.testing.assert_allclose(oe.z, w.rvec, atol=1e-8 * np.linalg.norm(w.b))
@@ -91,11 +91,31 @@ def test_exact_mode_limits_and_fewer_iterations():
     assert it_e < it_p
 
 
+@pytest.mark.parametrize("noise", [0.0, 0.2])
+def test_inner_cgls_mode_converges_to_the_projection(noise):
+    # the paper's route (inner LSQR-equivalent CGLS, update="exact") reaches the
+    # pseudoinverse updates (update="exact_lstsq") on well-conditioned blocks
+    w = dense_gaussian(150, 40, seed=9, noise=noise)
+    oc = Oracle(w.A, w.b, 0.5, update="exact", inner_tol=1e-14, inner_max=300)
+    ol = Oracle(w.A, w.b, 0.5, update="exact_lstsq")
+    for _ in range(6):
+        rc, rl = oc.iterate(8), ol.iterate(8)
+        assert (rc.hash_u, rc.hash_j) == (rl.hash_u, rl.hash_j)
+        assert np.linalg.norm(oc.x - ol.x) <= 1e-10 * np.linalg.norm(ol.x)
+        assert np.linalg.norm(oc.z - ol.z) <= 1e-10 * np.linalg.norm(w.b)
+    # one inner iteration of the z-solve is exactly the pseudoinverse-free z-step
+    o1 = Oracle(w.A, w.b, 0.5, update="exact", inner_max=1)
+    op = Oracle(w.A, w.b, 0.5)
+    o1.column_step(2)
+    op.column_step(2)
+    np.testing.assert_array_equal(o1.z, op.z)
+
+
 def test_exact_mode_sprandn_fat_iteration_count():
     # on a 1 %-dense 500 x 8000 sprandn-like system at eta = 0.5, RSE <= 1e-6,
     # exact projections took 6 iterations against 15 for the pinv-free sweep (paper: 12.0)
     w = sparse_random(500, 8000, density=0.01, seed=0)
-    oe = Oracle(w.A, w.b, 0.5, update="exact")
+    oe = Oracle(w.A, w.b, 0.5, update="exact_lstsq")
     out, it_e, rse, _ = oe.solve(1e-6, 200, 1, stop=STOP_RSE)
     op = Oracle(w.A, w.b, 0.5)
     out2, it_p, rse2, _ = op.solve(1e-6, 500, 1, stop=STOP_RSE)
