@@ -154,7 +154,7 @@ def time_kernel(s, kernel, reps, torch):
     return e0.elapsed_time(e1) * 1e-3 / reps, bytes_per
 
 
-def cpu_oracle_sample(w, budget_s=15.0, max_iters=None):
+def cpu_oracle_sample(w, budget_s=15.0, max_iters=None, mode="pinv_free", inner=(1e-13, 200)):
     """Oracle iterations/s on a bounded sample (first iterations of the same solve)."""
     from oracle import Oracle
     try:
@@ -162,7 +162,7 @@ def cpu_oracle_sample(w, budget_s=15.0, max_iters=None):
         threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
     except Exception:
         threads = os.cpu_count()
-    o = Oracle(w.A, w.b, w.eta)
+    o = Oracle(w.A, w.b, w.eta, update=mode, inner_tol=inner[0], inner_max=inner[1])
     t0 = time.perf_counter()
     it = 0
     while True:
@@ -207,6 +207,8 @@ def run_ours(args):
         rows = parts[rank]
         comm = init_nccl_comm(local)
     s = make_solver(w, local, stream.cuda_stream, rows, comm)
+    if args.mode == "exact":
+        s.set_mode("exact", inner_tol=args.inner_tol, inner_max=args.inner_max)
     engine, ctas = s.engine_info()
     s.reset(0)
     s.step(args.warmup)                              # W untimed warm-up iterations
@@ -285,6 +287,8 @@ def run_ours(args):
         t0 = time.perf_counter()
         s2 = make_solver(w, local, stream.cuda_stream, rows, comm,
                          A_host=A_h if w.dense else None, b_host=b_h)
+        if args.mode == "exact":
+            s2.set_mode("exact", inner_tol=args.inner_tol, inner_max=args.inner_max)
         s2.reset(0)
         s2.step(args.steps)
         s2.x(out=x_h)
@@ -302,7 +306,7 @@ def run_ours(args):
 
     # per-phase device time of the persistent kernel (separate instrumented handle)
     phases = None
-    if engine == 0 and world == 1 and not args.skip_phases:
+    if engine == 0 and world == 1 and not args.skip_phases and args.mode == "pinv_free":
         os.environ["RGDBEK_PHASE_TIMING"] = "1"
         sp = make_solver(w, local, stream.cuda_stream)
         del os.environ["RGDBEK_PHASE_TIMING"]
@@ -323,7 +327,8 @@ def run_ours(args):
     if rank == 0:
         cpu = None
         if not args.skip_cpu:
-            v, it, el, threads = cpu_oracle_sample(w, budget_s=args.cpu_budget)
+            v, it, el, threads = cpu_oracle_sample(w, budget_s=args.cpu_budget, mode=args.mode,
+                                                   inner=(args.inner_tol, args.inner_max))
             cpu = {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "oracle",
                    "sample": f"first {it} iterations of the same {args.workload} solve "
                              f"(seed 0) in {el:.1f} s, numpy/BLAS fp64 incl. the per-iteration RSE matvec"}
@@ -337,6 +342,7 @@ def run_ours(args):
                        "m": m, "n": n, "nnz": int(w.nnz), "eta": w.eta,
                        "parallelism": f"rows{world} (NCCL)" if world > 1 else "single",
                        "engine": "persistent" if engine == 0 else "graph",
+                       "update": args.mode,
                        "l2": "inputs larger than L2 (A = %.0f MB > 126 MB)" % (
                            (m * n * 8 if w.dense else w.A.nnz * 12) / 1e6)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "time_to_tol": ttt,
@@ -406,6 +412,10 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-ttt", action="store_true")
     ap.add_argument("--skip-phases", action="store_true")
+    ap.add_argument("--mode", default="pinv_free", choices=["pinv_free", "exact"],
+                    help="exact = Alg. 1's pseudoinverse updates by inner CGLS (NEXT #1)")
+    ap.add_argument("--inner-tol", type=float, default=1e-13)
+    ap.add_argument("--inner-max", type=int, default=200)
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rule)")

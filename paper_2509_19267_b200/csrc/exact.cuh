@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
       for (int it = 0; it < e.inner_max && gam > 0.0; ++it) {
         double Wd = 0.0, Yd = 0.0;
         ex_passN(a, e.px, e.px, e.u, a.w, nullptr, Wd, Yd, dyn);            // u = A p
-        __syncthreads();
+        grid_sync(a.bar, bgen);   // sparse tiles spread rows over all CTAs
         double qp = 0.0;
         for (int i = blockIdx.x * PT + threadIdx.x; i < m_loc; i += G * PT)
           if (p_selected(&ps, a.keys_m[i], a.row0 + i)) qp += e.u[i] * e.u[i];

@@ -325,11 +325,15 @@ def test_time_to_tolerance_c5s_scaled_twin():
     s.close()
 
 
-@pytest.mark.parametrize("name,inner_max", [("C2s", 200), ("C2si", 200), ("C5t", 100), ("C3s", 60)])
+@pytest.mark.parametrize("name,inner_max", [("C2s", 200), ("C2si", 200), ("C5t", 2000), ("C3s", 60)])
 def test_exact_projection_mode(name, inner_max):
     """NEXT #1: Alg. 1's exact projections by inner CGLS (the paper's
     LSQR route), same stopping rule on both sides: identical blocks every
-    iteration, x and z to 1e-8."""
+    iteration, x and z to 1e-8.  inner_max lets the inner solves converge
+    (C5t's row blocks have kappa ~ 43, so CGLS needs ~10^3 iterations to 1e-13):
+    an UNconverged Krylov iterate on an ill-conditioned block amplifies the
+    two sides' different summation orders, so only converged solves are compared
+    (C3s runs a fixed 60 inner iterations on well-separated blocks)."""
     from oracle import Oracle
     from workloads import by_name
     w = by_name(name)
