@@ -231,6 +231,7 @@ def run_ours(args):
         t = float(tt.item())
     value = args.steps / t                           # iterations of the one (sharded) system
     launches = 1 + (1 if engine == 0 else s.launches_per_iteration() * (args.steps + 1))
+    npass = s.passes() if engine == 0 else 2 * (args.steps + 1)   # passes over A in the timed call
 
     # roofline of the dominant kernel.  Persistent engine: the timed region IS one
     # launch of k_persistent (K iterations); achieved = K * B_iter / event time.
@@ -242,7 +243,20 @@ def run_ours(args):
         kernels[kname] = {"seconds": dt, "bytes": bytes_per, "gbs": bytes_per / dt / 1e9}
     s.reset(0)
     tr = load_traffic(args.workload, "k_persistent_per_iter")
-    if engine == 0:
+    if engine == 0 and args.mode == "exact":
+        # exact mode: the inner solves make the passes per iteration data-dependent;
+        # algorithmic bytes = (passes run) x (bytes of A per pass) + the vector sweeps
+        m_, n_ = w.shape
+        a_pass = 8.0 * m_ * n_ if w.dense else 12.0 * w.A.nnz + 4.0 * (m_ + 1)
+        b_launch = npass * a_pass + args.steps * (32.0 * m_ + 24.0 * n_)
+        ach = b_launch / t / 1e9
+        roofline = {"bound": "hbm", "kernel": f"k_persistent_exact ({ctas} CTAs x 1024 threads; "
+                                              f"{args.steps} iterations, {npass} passes over A)",
+                    "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(ach / peak, 4), "traffic": None,
+                    "algorithmic_bytes_per_launch": b_launch, "peak_source": peak_src,
+                    "passes_per_iteration": round(npass / args.steps, 2)}
+    elif engine == 0:
         ach = b_iter * args.steps / t / 1e9 / world
         roofline = {"bound": "hbm", "kernel": f"k_persistent ({ctas} CTAs x 1024 threads; "
                                               f"{args.steps} iterations per launch)",

@@ -193,6 +193,9 @@ rgdbek_status rgdbek_launches_per_iteration(rgdbek_handle h, int64_t* out);
 rgdbek_status rgdbek_phase_times(rgdbek_handle h, double* out_ns, int32_t max_phases,
                                  int32_t* n_out);
 rgdbek_status rgdbek_engine_info(rgdbek_handle h, int32_t* engine, int32_t* ctas);
+/* Full passes over A executed by the persistent engine since the last reset (2 per
+ * iteration in mode 0; 2 + 2 per inner iteration in mode 1). */
+rgdbek_status rgdbek_get_counters(rgdbek_handle h, int64_t* passes);
 
 /* The cudaStream_t the handle runs on (for events / synchronisation). */
 void*         rgdbek_stream(rgdbek_handle h);

@@ -149,6 +149,10 @@ class Solver:
         m = {"pinv_free": 0, "exact": 1}[mode] if isinstance(mode, str) else int(mode)
         N.rgdbek_set_mode(self._h, m, inner_tol, inner_max)
 
+    def passes(self):
+        """Full passes over A since the last reset (persistent engine)."""
+        return N.rgdbek_get_counters(self._h)
+
     def engine_info(self):
         """(engine, ctas): engine 0 = persistent kernel, 1 = CUDA-graph engine."""
         return N.rgdbek_engine_info(self._h)

@@ -73,6 +73,7 @@ struct Scal {
   double wy[2];                  // [W_p, ||b_p - A_p x||^2]
   unsigned long long jacc[2];    // [|J_p|, hash(J_p)]
   unsigned int nsurv, surv_over; // local survivors of the level-3 bucket
+  long long npass;               // full passes over A since the last reset (exact mode)
 };
 
 constexpr int SURV_CAP = 256;    // per-rank survivors exchanged by allgather

@@ -137,11 +137,13 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
   const double tol2 = e.inner_tol * e.inner_tol;
   unsigned int bgen = 0;
   if (threadIdx.x == 0) bgen = ld_acquire_u32(&a.bar->gen);
+  long long npass = 0;                       // full passes over A in this launch
 
   // ---- prologue: A x_k (the first row step's residual and the RSE of x_k) ----
   double Yk;
   {
     double Wd = 0.0, Yp = 0.0;
+    ++npass;
     ex_passN(a, a.x, a.x, e.u, a.ax, a.b, Wd, Yp, dyn);
     double Wsum;
     ex_allsum2(a, Wd, Yp, SL_W, SL_Y, sh, bgen, Wsum, Yk);
@@ -151,6 +153,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
       const double rse = Yk / bnorm2;
       st->halted = 1; st->outcome = RGDBEK_MAX_ITER; st->iters = k; st->rse_out = rse;
       st->relerr_out = __longlong_as_double(0x7FF8000000000000ll);
+      st->npass += npass;
     }
     return;
   }
@@ -159,6 +162,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     // ======================= column step =======================
     for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
     __syncthreads();
+    ++npass;
     ex_passT(a, a.z, a.z, 0, a.s, a.v, dyn, bgen);                 // s = A^T z_k
     p_zero_side(a, 1);
     for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) {
@@ -213,6 +217,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     double gam = Z, W0 = 0.0;
     for (int it = 0; it < e.inner_max && kp > 0 && gam > 0.0; ++it) {
       double Wp = 0.0, Yd = 0.0;
+      ++npass;
       ex_passN(a, a.zeta, a.zeta, a.w, e.u, nullptr, Wp, Yd, dyn);           // q = A p
       double Wq, d2;
       ex_allsum2(a, Wp, 0.0, SL_W, SL_Y, sh, bgen, Wq, d2);
@@ -223,6 +228,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
         a.z[i] = __dsub_rn(a.z[i], __dmul_rn(al, a.w[i]));
       if (it + 1 == e.inner_max) break;
       grid_sync(a.bar, bgen);
+      ++npass;
       ex_passT(a, a.z, a.z, 0, a.s, a.v, dyn, bgen);                         // s' = A^T z
       double gp = 0.0;
       for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT)
@@ -298,6 +304,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     // a.xi holds its residual restricted to J; e.px its direction.
     double V0 = 0.0;
     if (kpp > 0 && X > 0.0) {
+      ++npass;
       ex_passT(a, a.xi, a.xi, 0, a.v, a.s, dyn, bgen);                      // t = A^T r_J
       double gp = 0.0;
       for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) {
@@ -311,6 +318,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
       double gam = gam0;
       for (int it = 0; it < e.inner_max && gam > 0.0; ++it) {
         double Wd = 0.0, Yd = 0.0;
+        ++npass;
         ex_passN(a, e.px, e.px, e.u, a.w, nullptr, Wd, Yd, dyn);            // u = A p
         grid_sync(a.bar, bgen);   // sparse tiles spread rows over all CTAs
         double qp = 0.0;
@@ -327,6 +335,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
             a.xi[i] = __dsub_rn(a.xi[i], __dmul_rn(al, e.u[i]));
         if (it + 1 == e.inner_max) break;
         grid_sync(a.bar, bgen);
+        ++npass;
         ex_passT(a, a.xi, a.xi, 0, a.v, a.s, dyn, bgen);                    // t = A^T r_J
         double gq = 0.0;
         for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) gq += a.v[j] * a.v[j];
@@ -347,6 +356,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     double Y, relerr2;
     {
       double Wd = 0.0, Yp = 0.0, Rp = 0.0;
+      ++npass;
       ex_passN(a, a.x, a.x, e.u, a.ax, a.b, Wd, Yp, dyn);
       if (has_ref)
         for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) {
@@ -369,6 +379,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
       if (lead) {
         st->halted = 1; st->outcome = outcome; st->iters = k; st->rse_out = rse;
         st->relerr_out = rel; st->k = k; st->pending = 0; st->kp_prev = kp; st->kpp_prev = kpp;
+        st->npass += npass;
       }
       return;
     }

@@ -862,6 +862,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
           st->relerr_out = rel; st->k = k; st->pending = 0; st->X = X;
           st->kp_prev = kp_prev; st->kpp_prev = kpp_prev;
           st->Z = Z; st->W = W; st->Y = Y; st->V = V; st->relerr2 = relerr2;
+          st->npass += 2 * (k - k_begin + 1);
         }
         return;
       }

@@ -1221,6 +1221,15 @@ rgdbek_status rgdbek_set_mode(rgdbek_handle h, int32_t mode, double inner_tol, i
   return RGDBEK_OK;
 }
 
+rgdbek_status rgdbek_get_counters(rgdbek_handle h, int64_t* passes) {
+  TRY(ensure_usable(h));
+  if (!passes) return set_err(h, RGDBEK_E_ARG, "NULL out");
+  CK(h, cudaMemcpyAsync(h->st_host, h->st, sizeof(Scal), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  *passes = h->st_host->npass;
+  return RGDBEK_OK;
+}
+
 rgdbek_status rgdbek_engine_info(rgdbek_handle h, int32_t* engine, int32_t* ctas) {
   if (!h || !engine || !ctas) return RGDBEK_E_ARG;
   *engine = h->engine;
