@@ -157,6 +157,14 @@ rgdbek_status rgdbek_set_stop(rgdbek_handle h, int32_t stop);
  * residual has dropped by inner_tol (relative) or after inner_max iterations.  mode 1 needs the
  * single-GPU persistent engine (RGDBEK_E_STATE otherwise). */
 rgdbek_status rgdbek_set_mode(rgdbek_handle h, int32_t mode, double inner_tol, int32_t inner_max);
+
+/* Block selection rule.  0 (default): RGDBEK's randomized sampling of
+ * eta*n columns / eta*m rows with P(j) proportional to the residual scores (P:93-100,
+ * Alg. 1 lines 4-7 and 9-12).  1: GDBEK's greedy threshold sets
+ *   U = {j : eps^z_j >= eta * max eps^z},  J = {i : eps^x_i >= eta * max eps^x}
+ * (no sampling; block sizes vary).  Combine with rgdbek_set_mode(1) for GDBEK's
+ * pseudoinverse updates (eq:updateGDBEK).  Needs the single-GPU persistent engine. */
+rgdbek_status rgdbek_set_selection(rgdbek_handle h, int32_t selection);
 rgdbek_status rgdbek_set_reference(rgdbek_handle h, const double* xstar /* n values */);
 
 rgdbek_status rgdbek_get_x(rgdbek_handle h, double* out_n);

@@ -128,6 +128,15 @@ def select_block(kappa, kk, eligible=None):
     return np.sort(order[:kk])
 
 
+def greedy_block(eps, eta):
+    """GDBEK's greedy set {j : eps_j >= eta * max_l eps_l} (P:84-90), '>=' per SPEC S:303;
+    empty when every score is 0."""
+    emax = float(eps.max()) if len(eps) else 0.0
+    if not emax > 0:
+        return np.zeros(0, dtype=np.int64)
+    return np.flatnonzero(eps >= eta * emax)
+
+
 @dataclass
 class IterRecord:
     """What one iteration k produced (compared with the GPU trace)."""
@@ -148,9 +157,13 @@ class IterRecord:
 class Oracle:
     """State (x_k, z_k, k) of Algorithm 1 and its plain iteration."""
 
-    def __init__(self, A, b, eta=0.5, update="pinv_free", inner_tol=1e-13, inner_max=50):
+    def __init__(self, A, b, eta=0.5, update="pinv_free", inner_tol=1e-13, inner_max=50,
+                 select="random"):
         if update not in ("pinv_free", "exact", "exact_lstsq"):
             raise ValueError("update must be 'pinv_free', 'exact' or 'exact_lstsq'")
+        if select not in ("random", "greedy"):
+            raise ValueError("select must be 'random' or 'greedy'")
+        self.select = select
         self.update = update
         self.inner_tol = float(inner_tol)
         self.inner_max = int(inner_max)
@@ -185,9 +198,13 @@ class Oracle:
         A, z = self.A, self.z
         s = A.T @ z                                        # A^T z_k
         eps = scores(s, self.gamma)                        # eps^z
-        kappa = sample_keys(eps, seed, self.k, 0)
-        kp = min(self.kc, int(np.count_nonzero(eps > 0)))  # clamp (reading R6)
-        U = select_block(kappa, kp, eps > 0)
+        if self.select == "greedy":
+            U = greedy_block(eps, self.eta)                # GDBEK threshold set
+            kp = len(U)
+        else:
+            kappa = sample_keys(eps, seed, self.k, 0)
+            kp = min(self.kc, int(np.count_nonzero(eps > 0)))  # clamp (reading R6)
+            U = select_block(kappa, kp, eps > 0)
         zeta = np.zeros(self.n)
         zeta[U] = s[U]
         Z = float(s[U] @ s[U])
@@ -236,9 +253,13 @@ class Oracle:
         A = self.A
         r = self.b - self.z - A @ self.x                   # uses z_{k+1} (reading R8)
         eps = scores(r, self.rho)                          # eps^x
-        kappa = sample_keys(eps, seed, self.k, 1)
-        kpp = min(self.kr, int(np.count_nonzero(eps > 0)))
-        J = select_block(kappa, kpp, eps > 0)
+        if self.select == "greedy":
+            J = greedy_block(eps, self.eta)
+            kpp = len(J)
+        else:
+            kappa = sample_keys(eps, seed, self.k, 1)
+            kpp = min(self.kr, int(np.count_nonzero(eps > 0)))
+            J = select_block(kappa, kpp, eps > 0)
         xi = np.zeros(self.m)
         xi[J] = r[J]
         X = float(r[J] @ r[J])

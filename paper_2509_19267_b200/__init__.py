@@ -149,6 +149,11 @@ class Solver:
         m = {"pinv_free": 0, "exact": 1}[mode] if isinstance(mode, str) else int(mode)
         N.rgdbek_set_mode(self._h, m, inner_tol, inner_max)
 
+    def set_selection(self, rule):
+        """'random' (RGDBEK sampling, default) or 'greedy' (GDBEK threshold sets)."""
+        r = {"random": 0, "greedy": 1}[rule] if isinstance(rule, str) else int(rule)
+        N.rgdbek_set_selection(self._h, r)
+
     def passes(self):
         """Full passes over A since the last reset (persistent engine)."""
         return N.rgdbek_get_counters(self._h)

@@ -18,7 +18,7 @@ namespace rg {
 constexpr unsigned long long KEY_NEVER = 0xFFFFFFFFFFFFFFFFull;
 
 // Selection modes (SelState::mode)
-enum : int { SEL_NONE = 0, SEL_ALL = 1, SEL_THRESH = 2, SEL_PENDING = 3 };
+enum : int { SEL_NONE = 0, SEL_ALL = 1, SEL_THRESH = 2, SEL_PENDING = 3, SEL_GREEDY = 4 };
 
 // Radix levels of the exact k-th key search: L1 = key >> 52 (sign+exponent,
 // 4096 bins, fused into the key-producing kernel), L2 = bits [51:40],
@@ -124,6 +124,15 @@ __device__ __forceinline__ unsigned long long make_key(double eps, unsigned long
   const double u = u01(c0, c1);
   const double kappa = __ddiv_rn(-log(u), eps);
   return (unsigned long long)__double_as_longlong(kappa);
+}
+
+// Selection key of one score: the Philox exponential key (RGDBEK) or, in
+// the greedy GDBEK mode, the score's own bits.
+__device__ __forceinline__ unsigned long long sel_key(double eps, unsigned long long gidx,
+                                                      long long k, uint32_t step,
+                                                      unsigned long long seed, int greedy) {
+  if (greedy) return eps > 0.0 ? (unsigned long long)__double_as_longlong(eps) : KEY_NEVER;
+  return make_key(eps, gidx, k, step, seed);
 }
 
 __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {

@@ -45,14 +45,16 @@ struct ColKeyEpi {
   long long k;
   unsigned long long seed;
   int pending;
+  int greedy;
 };
 
 __device__ __forceinline__ void colkey_epilogue(const ColKeyEpi* ep, int j, double sj, double vj,
-                                                double& Vp) {
+                                                double& Vp, double& Emax) {
   if (ep->pending) Vp += vj * vj;
   const double g = ep->gamma[j];
   const double eps = g > 0.0 ? __ddiv_rn(__dmul_rn(sj, sj), g) : 0.0;
-  const unsigned long long key = make_key(eps, (unsigned long long)j, ep->k, 0u, ep->seed);
+  Emax = fmax(Emax, eps);
+  const unsigned long long key = sel_key(eps, (unsigned long long)j, ep->k, 0u, ep->seed, ep->greedy);
   ep->keys[j] = key;
   atomicAdd(&ep->hist[key >> L1_SHIFT], 1u);
 }
@@ -93,7 +95,7 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
           Wp += s1 * s1;
           Yp += y * y;
         }
-        if (ep) colkey_epilogue(ep, r0, s1, s2, Wp);
+        if (ep) colkey_epilogue(ep, r0, s1, s2, Wp, Yp);
         if (acc1) Wp += s1 * s1;
       }
       group_bar(bar_id);
@@ -140,7 +142,7 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
         Wp += s1 * s1;
         Yp += y * y;
       }
-      if (ep) colkey_epilogue(ep, r0 + r, s1, s2, Wp);
+      if (ep) colkey_epilogue(ep, r0 + r, s1, s2, Wp, Yp);
       if (acc1) Wp += s1 * s1;
     }
     group_bar(bar_id);

@@ -165,21 +165,30 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     ++npass;
     ex_passT(a, a.z, a.z, 0, a.s, a.v, dyn, bgen);                 // s = A^T z_k
     p_zero_side(a, 1);
+    double Emax = 0.0;
     for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) {
       const double sj = a.s[j];
       const double gm = a.gamma[j];
       const double eps = gm > 0.0 ? __ddiv_rn(__dmul_rn(sj, sj), gm) : 0.0;
-      const unsigned long long key = make_key(eps, (unsigned long long)j, k, 0u, seed);
+      Emax = fmax(Emax, eps);
+      const unsigned long long key = sel_key(eps, (unsigned long long)j, k, 0u, seed, a.greedy);
       a.keys_n[j] = key;
       atomicAdd(&h[key >> L1_SHIFT], 1u);
     }
     __syncthreads();
     flush_hist<PT>(h, hn, NBINS);
+    {
+      const double eb = pblock_max(Emax, sh);
+      if (threadIdx.x == 0) bp[SL_MAXN * G + blockIdx.x] = eb;
+    }
     grid_sync(a.bar, bgen);
-    p_sel_level1(&ps, hn, n, kc, sh_u, sh_l);
-    if (n <= LOCAL_SEL_MAX) {
+    if (a.greedy) {
+      p_sel_greedy(&ps, slot_max(bp, SL_MAXN, sh), a.eta);
+    } else if (n <= LOCAL_SEL_MAX) {
+      p_sel_level1(&ps, hn, n, kc, sh_u, sh_l);
       p_sel_local(&ps, a.keys_n, n, 0, h, sh_u, sh_l);
     } else {
+      p_sel_level1(&ps, hn, n, kc, sh_u, sh_l);
       p_sel_scan<2>(&ps, a.keys_n, n, 0, hn + NBINS, cn, a.ncand, h);
       grid_sync(a.bar, bgen);
       p_sel_level2(&ps, hn + NBINS, sh_u, sh_l);
@@ -210,7 +219,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     const long long kp = (long long)__ldcg(&a.acc[0]);
     const unsigned long long hashU = __ldcg(&a.acc[1]);
     if (lead) {
-      if (kp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 1;
+      if (!a.greedy && kp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 1;
       if (TraceRec* t = trace_at(tr, st, k)) { t->k = k; t->kp = kp; t->hash_u = hashU; t->Z = Z; }
     }
     // CGLS on min ||A_U y - z_k||: z is its residual
@@ -249,22 +258,31 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     // ======================= row step =======================
     for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
     __syncthreads();
+    double EmaxM = 0.0;
     for (int i = blockIdx.x * PT + threadIdx.x; i < m_loc; i += G * PT) {
       const double ri = __dsub_rn(__dsub_rn(a.b[i], a.z[i]), a.ax[i]);
       a.r[i] = ri;
       const double p = a.rho[i];
       const double eps = p > 0.0 ? __ddiv_rn(__dmul_rn(ri, ri), p) : 0.0;
-      const unsigned long long key = make_key(eps, (unsigned long long)(a.row0 + i), k, 1u, seed);
+      EmaxM = fmax(EmaxM, eps);
+      const unsigned long long key = sel_key(eps, (unsigned long long)(a.row0 + i), k, 1u, seed, a.greedy);
       a.keys_m[i] = key;
       atomicAdd(&h[key >> L1_SHIFT], 1u);
     }
     __syncthreads();
     flush_hist<PT>(h, hm, NBINS);
+    {
+      const double eb = pblock_max(EmaxM, sh);
+      if (threadIdx.x == 0) bp[SL_MAXM * G + blockIdx.x] = eb;
+    }
     grid_sync(a.bar, bgen);
-    p_sel_level1(&ps, hm, m_loc, kr, sh_u, sh_l);
-    if (m_loc <= LOCAL_SEL_MAX) {
+    if (a.greedy) {
+      p_sel_greedy(&ps, slot_max(bp, SL_MAXM, sh), a.eta);
+    } else if (m_loc <= LOCAL_SEL_MAX) {
+      p_sel_level1(&ps, hm, m_loc, kr, sh_u, sh_l);
       p_sel_local(&ps, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
     } else {
+      p_sel_level1(&ps, hm, m_loc, kr, sh_u, sh_l);
       p_sel_scan<2>(&ps, a.keys_m, m_loc, a.row0, hm + NBINS, cm, a.ncand + 1, h);
       grid_sync(a.bar, bgen);
       p_sel_level2(&ps, hm + NBINS, sh_u, sh_l);
@@ -297,7 +315,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     const long long kpp = (long long)__ldcg(&a.acc[2]);
     const unsigned long long hashJ = __ldcg(&a.acc[3]);
     if (lead) {
-      if (kpp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 2;
+      if (!a.greedy && kpp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 2;
       if (TraceRec* t = trace_at(tr, st, k)) { t->kpp = kpp; t->hash_j = hashJ; t->X = X; }
     }
     // CGLS on min ||A^J y - r^J|| from y = 0 (limit: (A^J)^+ r^J): x += y.

@@ -31,7 +31,7 @@ struct GridBar {
   unsigned int pad1[31];
 };
 
-enum : int { SL_V = 0, SL_Z, SL_R, SL_W, SL_Y, SL_X, SL_NUM };
+enum : int { SL_V = 0, SL_Z, SL_R, SL_W, SL_Y, SL_X, SL_MAXN, SL_MAXM, SL_NUM };
 
 struct PArgs {
   int dense, m_loc, n, vecN, vecT, Q, CH;
@@ -54,6 +54,8 @@ struct PArgs {
   unsigned long long* ptime;        // optional per-phase device time (ns), [16]
   const int* tilesN; const int* tilesT;
   int ntilesN, ntilesT;
+  int greedy;                       // 1 = GDBEK threshold sets instead of sampling
+  double eta;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -116,6 +118,31 @@ __device__ __forceinline__ double slot_sum(const double* bpart, int slot, double
   return pblock_sum(t, sh);
 }
 
+// Block / grid maxima (greedy mode): fmax is order-independent, hence identical everywhere.
+__device__ __forceinline__ double pblock_max(double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double t = (threadIdx.x < 32 && l < PW) ? sh[l] : 0.0;
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
+    if (l == 0) sh[0] = t;
+  }
+  __syncthreads();
+  t = sh[0];
+  __syncthreads();
+  return t;
+}
+__device__ __forceinline__ double slot_max(const double* bpart, int slot, double* sh) {
+  double t = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += PT) t = fmax(t, __ldcg(bpart + slot * gridDim.x + i));
+  return pblock_max(t, sh);
+}
+
 // Bucket holding the need-th (1-based) count of a global histogram.  All
 // threads return (digit, count strictly below).  Redundant in every CTA.
 __device__ void p_find_bucket(const unsigned int* gh, long long need, unsigned int* sh_u,
@@ -172,7 +199,18 @@ struct PSel {
   unsigned long long prefix, tau;
   long long below, target, npos, tie;
   int mode, slow;
+  double thr;                  // greedy: select eps >= thr = eta * max eps
 };
+
+// GDBEK threshold set {i : eps_i >= eta * max eps} (>= per SPEC S:303).
+__device__ __forceinline__ void p_sel_greedy(PSel* ps, double emax, double eta) {
+  if (threadIdx.x == 0) {
+    ps->mode = emax > 0.0 ? SEL_GREEDY : SEL_NONE;
+    ps->thr = eta * emax;
+    ps->target = -1;
+  }
+  __syncthreads();
+}
 
 // Level-1 finalize: block size clamp and first bucket.
 __device__ void p_sel_level1(PSel* ps, const unsigned int* gh, long long N, long long kblock,
@@ -424,6 +462,7 @@ __device__ void p_sel_local(PSel* ps, const unsigned long long* __restrict__ key
 
 __device__ __forceinline__ bool p_selected(const PSel* ps, unsigned long long key, long long gidx) {
   if (ps->mode == SEL_THRESH) return key < ps->tau || (key == ps->tau && gidx <= ps->tie);
+  if (ps->mode == SEL_GREEDY) return key != KEY_NEVER && __longlong_as_double((long long)key) >= ps->thr;
   if (ps->mode == SEL_ALL) return key != KEY_NEVER;
   return false;
 }
@@ -673,7 +712,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     // ===== P1: pass T  (s_k = A^T z_k, v_{k-1} = A^T xi_{k-1}) =====
     // Sparse: the column scores, keys, level-1 histogram and V partial are fused
     // into the tile epilogue, so the separate P2 phase (and its barrier) vanishes.
-    double Vp = 0.0;
+    double Vp = 0.0, Emax = 0.0;
     if (a.dense) {
       p_dense_passT(a, pending, dyn);
       grid_sync(a.bar, bgen);
@@ -725,7 +764,8 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
             if (pending) Vp += tv * tv;
             const double gm = a.gamma[j];
             const double eps = gm > 0.0 ? __ddiv_rn(__dmul_rn(ts, ts), gm) : 0.0;
-            const unsigned long long key = make_key(eps, (unsigned long long)j, k, 0u, seed);
+            Emax = fmax(Emax, eps);
+            const unsigned long long key = sel_key(eps, (unsigned long long)j, k, 0u, seed, a.greedy);
             a.keys_n[j] = key;
             atomicAdd(&h[key >> L1_SHIFT], 1u);
           }
@@ -737,7 +777,8 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       flush_hist<PT>(h, hn, NBINS);
       {
         const double vb = pblock_sum(Vp, sh);
-        if (threadIdx.x == 0) bp[SL_V * G + blockIdx.x] = vb;
+        const double eb = pblock_max(Emax, sh);
+        if (threadIdx.x == 0) { bp[SL_V * G + blockIdx.x] = vb; bp[SL_MAXN * G + blockIdx.x] = eb; }
       }
       PH(12);
       grid_sync(a.bar, bgen);
@@ -745,17 +786,17 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     } else {
       for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
       __syncthreads();
-      double dummyY = 0.0;
-      const ColKeyEpi ep{a.gamma, a.keys_n, h, k, seed, pending};
+      const ColKeyEpi ep{a.gamma, a.keys_n, h, k, seed, pending, a.greedy};
       const int g = threadIdx.x / TG;
       csr_tiles(blockIdx.x * (PT / TG) + g, G * (PT / TG), threadIdx.x % TG, 1 + g,
                 reinterpret_cast<TileSmem*>(dyn) + g, a.cp, a.ri, a.rv, a.tilesT, a.ntilesT,
-                a.z, a.xi, pending, nullptr, a.s, a.v, Vp, dummyY, &ep);
+                a.z, a.xi, pending, nullptr, a.s, a.v, Vp, Emax, &ep);
       __syncthreads();
       flush_hist<PT>(h, hn, NBINS);
       {
         const double vb = pblock_sum(Vp, sh);
-        if (threadIdx.x == 0) bp[SL_V * G + blockIdx.x] = vb;
+        const double eb = pblock_max(Emax, sh);
+        if (threadIdx.x == 0) { bp[SL_V * G + blockIdx.x] = vb; bp[SL_MAXN * G + blockIdx.x] = eb; }
       }
       grid_sync(a.bar, bgen);
       PH(1);
@@ -769,10 +810,13 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     if (lead && pending) {
       if (TraceRec* t = trace_at(tr, st, k - 1)) t->V = V;
     }
-    p_sel_level1(&ps, hn, n, kc, sh_u, sh_l);
-    if (n <= LOCAL_SEL_MAX) {
+    if (a.greedy) {
+      p_sel_greedy(&ps, slot_max(bp, SL_MAXN, sh), a.eta);
+    } else if (n <= LOCAL_SEL_MAX) {
+      p_sel_level1(&ps, hn, n, kc, sh_u, sh_l);
       p_sel_local(&ps, a.keys_n, n, 0, h, sh_u, sh_l);
     } else {
+      p_sel_level1(&ps, hn, n, kc, sh_u, sh_l);
       p_sel_scan<2>(&ps, a.keys_n, n, 0, hn + NBINS, cn, a.ncand, h);
       grid_sync(a.bar, bgen);
       PH(3);
@@ -818,7 +862,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     const long long kp = (long long)__ldcg(&a.acc[0]);
     const unsigned long long hashU = __ldcg(&a.acc[1]);
     if (lead) {
-      if (kp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 1;
+      if (!a.greedy && kp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 1;
       if (TraceRec* t = trace_at(tr, st, k)) { t->k = k; t->kp = kp; t->hash_u = hashU; t->Z = Z; }
     }
     {
@@ -869,6 +913,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     }
     for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
     __syncthreads();
+    double EmaxM = 0.0;
     {
       const int doz = kp > 0 && W > 0.0;
       const double az = doz ? __ddiv_rn(Z, W) : 0.0;
@@ -879,22 +924,30 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
         a.r[i] = ri;
         const double p = a.rho[i];
         const double eps = p > 0.0 ? __ddiv_rn(__dmul_rn(ri, ri), p) : 0.0;
-        const unsigned long long key = make_key(eps, (unsigned long long)(a.row0 + i), k, 1u, seed);
+        EmaxM = fmax(EmaxM, eps);
+        const unsigned long long key = sel_key(eps, (unsigned long long)(a.row0 + i), k, 1u, seed, a.greedy);
         a.keys_m[i] = key;
         atomicAdd(&h[key >> L1_SHIFT], 1u);
       }
     }
     __syncthreads();
     flush_hist<PT>(h, hm, NBINS);
+    {
+      const double eb = pblock_max(EmaxM, sh);
+      if (threadIdx.x == 0) bp[SL_MAXM * G + blockIdx.x] = eb;
+    }
     p_zero_side(a, 0);                          // n-side buffers: consumed in P3..P6
     grid_sync(a.bar, bgen);
     PH(7);
 
     // ===== P9: level-1 bucket (J); level-2 scan =====
-    p_sel_level1(&ps, hm, m_loc, kr, sh_u, sh_l);
-    if (m_loc <= LOCAL_SEL_MAX) {
+    if (a.greedy) {
+      p_sel_greedy(&ps, slot_max(bp, SL_MAXM, sh), a.eta);
+    } else if (m_loc <= LOCAL_SEL_MAX) {
+      p_sel_level1(&ps, hm, m_loc, kr, sh_u, sh_l);
       p_sel_local(&ps, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
     } else {
+      p_sel_level1(&ps, hm, m_loc, kr, sh_u, sh_l);
       p_sel_scan<2>(&ps, a.keys_m, m_loc, a.row0, hm + NBINS, cm, a.ncand + 1, h);
       grid_sync(a.bar, bgen);
       PH(8);
@@ -935,7 +988,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     const long long kpp = (long long)__ldcg(&a.acc[2]);
     const unsigned long long hashJ = __ldcg(&a.acc[3]);
     if (lead) {
-      if (kpp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 2;
+      if (!a.greedy && kpp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 2;
       if (TraceRec* t = trace_at(tr, st, k)) { t->kpp = kpp; t->hash_j = hashJ; t->X = X; }
     }
     kp_prev = kp;

@@ -589,6 +589,8 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
   a.part = ppart; a.bpart = h->bpart; a.hist = h->phist; a.cand = h->pcand; a.acc = h->pacc;
   a.ncand = h->pncand; a.st = h->st; a.tr = h->trace; a.bar = h->pbar;
   a.tilesN = h->tilesN; a.tilesT = h->tilesT; a.ntilesN = h->ntilesN; a.ntilesT = h->ntilesT;
+  a.greedy = 0;
+  a.eta = h->eta;
   if (const char* e = getenv("RGDBEK_PHASE_TIMING")) {
     if (atoi(e)) {
       TRY(dalloc(h, &h->ptime, 16));
@@ -1218,6 +1220,15 @@ rgdbek_status rgdbek_set_mode(rgdbek_handle h, int32_t mode, double inner_tol, i
     h->eargs.inner_max = inner_max;
   }
   h->mode = mode;
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_set_selection(rgdbek_handle h, int32_t selection) {
+  TRY(ensure_usable(h));
+  if (selection < 0 || selection > 1) return set_err(h, RGDBEK_E_ARG, "unknown selection rule %d", selection);
+  if (selection == 1 && (h->engine != 0 || h->dist))
+    return set_err(h, RGDBEK_E_STATE, "greedy selection runs on the single-GPU persistent engine");
+  h->pargs.greedy = selection;
   return RGDBEK_OK;
 }
 

@@ -366,3 +366,30 @@ def test_exact_mode_time_to_tolerance():
     out, iters, _, _ = o.solve(1e-6, 1000, 0, stop=STOP_REL_ERR, xstar=w.xstar)
     assert res["outcome"] == RGDBEK_CONVERGED == out
     assert abs(res["iters"] - iters) <= max(1, int(0.02 * iters)), (res["iters"], iters)
+
+
+@pytest.mark.parametrize("name,update", [("C2s", "pinv_free"), ("C5t", "pinv_free"),
+                                         ("C3s", "pinv_free"), ("C2si", "exact")])
+def test_greedy_gdbek_selection(name, update):
+    """NEXT #2: GDBEK's threshold sets on the GPU (pinv-free and exact
+    updates) vs the oracle: identical blocks, x and z to 1e-10 (1e-8 exact)."""
+    from oracle import Oracle
+    from workloads import by_name
+    w = by_name(name)
+    s = _solver(w)
+    s.set_selection("greedy")
+    kw = {}
+    if update == "exact":
+        s.set_mode("exact", inner_tol=1e-13, inner_max=200)
+        kw = dict(update="exact", inner_tol=1e-13, inner_max=200)
+    o = Oracle(w.A, w.b, w.eta, select="greedy", **kw)
+    tol = 1e-8 if update == "exact" else TOL_X
+    s.reset(0)
+    for k in range(12):
+        rec = o.iterate(0)
+        s.step(1)
+        g = s.trace()[-1]
+        assert (g["kp"], g["hash_u"], g["kpp"], g["hash_j"]) == (rec.kp, rec.hash_u, rec.kpp, rec.hash_j), k
+        assert np.linalg.norm(s.x() - o.x) <= tol * np.linalg.norm(o.x), k
+        assert np.linalg.norm(s.z() - o.z) <= tol * np.linalg.norm(w.b), k
+    s.close()
