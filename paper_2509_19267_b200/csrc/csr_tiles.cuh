@@ -18,9 +18,9 @@
 
 namespace rg {
 
-constexpr int TG = 256;              // threads per worker group
-constexpr int TILE_NNZ = 2048;
-constexpr int TILE_ROWS = 512;
+constexpr int TG = 128;              // threads per worker group
+constexpr int TILE_NNZ = 1024;       // 8 nonzeros per thread, in two sub-rounds of 4
+constexpr int TILE_ROWS = 256;
 
 struct TileSmem {
   double p1[TILE_NNZ];
@@ -29,7 +29,7 @@ struct TileSmem {
   double red[2 * (TG / 32)];
 };
 
-// Barrier over this worker group's TG threads (id 0 == the whole 256-thread block).
+// Barrier over this worker group's TG threads (named barrier id >= 1).
 __device__ __forceinline__ void group_bar(int id) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(TG) : "memory");
 }
@@ -66,7 +66,7 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
                           const double* __restrict__ in2, int use2,
                           const double* __restrict__ b, double* __restrict__ o1,
                           double* __restrict__ o2, double& Wp, double& Yp,
-                          const ColKeyEpi* ep = nullptr, int acc1 = 0) {
+                          const ColKeyEpi* ep = nullptr, int acc1 = 0, int vec = 1) {
   for (int t = gid; t < ntiles; t += ngroups) {
     const int r0 = tiles[t], r1 = tiles[t + 1];
     const int nr = r1 - r0;
@@ -131,19 +131,34 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
       if (lt + (e0 + SUB) * TG >= nz) break;
     }
     group_bar(bar_id);
-    for (int r = lt; r < nr; r += TG) {
-      const int q0 = (int)(sm->rp[r] - p0), q1 = (int)(sm->rp[r + 1] - p0);
+    // row sums: vec lanes per row (power of two, chosen from the mean row length),
+    // strided partial sums then a fixed shuffle tree — deterministic; loop
+    // bounds are warp-uniform so the shuffles are well defined
+    const int lane = lt & 31, lw = lt >> 5;
+    const int spw = 32 / vec, sub = lane / vec, sl = lane & (vec - 1);
+    for (int base = lw * spw; base < nr; base += (TG / 32) * spw) {
+      const int r = base + sub;
+      const bool valid = r < nr;
       double s1 = 0.0, s2 = 0.0;
-      for (int q = q0; q < q1; ++q) { s1 += sm->p1[q]; s2 += sm->p2[q]; }
-      o1[r0 + r] = s1;
-      o2[r0 + r] = s2;
-      if (b) {
-        const double y = b[r0 + r] - s2;
-        Wp += s1 * s1;
-        Yp += y * y;
+      if (valid) {
+        const int q0 = (int)(sm->rp[r] - p0), q1 = (int)(sm->rp[r + 1] - p0);
+        for (int q = q0 + sl; q < q1; q += vec) { s1 += sm->p1[q]; s2 += sm->p2[q]; }
       }
-      if (ep) colkey_epilogue(ep, r0 + r, s1, s2, Wp, Yp);
-      if (acc1) Wp += s1 * s1;
+      for (int o = vec >> 1; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o, vec);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o, vec);
+      }
+      if (valid && sl == 0) {
+        o1[r0 + r] = s1;
+        o2[r0 + r] = s2;
+        if (b) {
+          const double y = b[r0 + r] - s2;
+          Wp += s1 * s1;
+          Yp += y * y;
+        }
+        if (ep) colkey_epilogue(ep, r0 + r, s1, s2, Wp, Yp);
+        if (acc1) Wp += s1 * s1;
+      }
     }
     group_bar(bar_id);
   }

@@ -78,7 +78,7 @@ __device__ void ex_passT(const PArgs& a, const double* in1, const double* in2, i
     const int g = threadIdx.x / TG;
     csr_tiles(blockIdx.x * (PT / TG) + g, gridDim.x * (PT / TG), threadIdx.x % TG, 1 + g,
               reinterpret_cast<TileSmem*>(dyn) + g, a.cp, a.ri, a.rv, a.tilesT, a.ntilesT, in1,
-              in2, use2, nullptr, o1, o2, d1, d2);
+              in2, use2, nullptr, o1, o2, d1, d2, nullptr, 0, a.vecT);
   }
   grid_sync(a.bar, bgen);
 }
@@ -93,7 +93,7 @@ __device__ void ex_passN(const PArgs& a, const double* in1, const double* in2, d
     const int g = threadIdx.x / TG;
     csr_tiles(blockIdx.x * (PT / TG) + g, gridDim.x * (PT / TG), threadIdx.x % TG, 1 + g,
               reinterpret_cast<TileSmem*>(dyn) + g, a.rp, a.ci, a.cv, a.tilesN, a.ntilesN, in1,
-              in2, 1, bvec, o1, o2, Wp, Yp, nullptr, bvec ? 0 : 1);
+              in2, 1, bvec, o1, o2, Wp, Yp, nullptr, bvec ? 0 : 1, a.vecN);
   }
 }
 

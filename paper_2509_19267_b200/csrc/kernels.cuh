@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(NT) k_csr_dual(const long long* __restrict__ p
 __device__ void passN_finish(Scal* st, TraceRec* tr, double* bpart, int nblk, double* sh);
 
 template <int MODE>
-__global__ void __launch_bounds__(TG) k_csr_tiles(const long long* __restrict__ ptr,
+__global__ void __launch_bounds__(NT) k_csr_tiles(const long long* __restrict__ ptr,
                                                  const int* __restrict__ idx,
                                                  const double* __restrict__ val,
                                                  const int* __restrict__ tiles, int ntiles,
@@ -254,18 +254,22 @@ __global__ void __launch_bounds__(TG) k_csr_tiles(const long long* __restrict__ 
                                                  const double* __restrict__ in2,
                                                  const double* __restrict__ b,
                                                  double* __restrict__ o1, double* __restrict__ o2,
-                                                 Scal* st, TraceRec* tr, double* bpart) {
+                                                 Scal* st, TraceRec* tr, double* bpart,
+                                                 int vec) {
   if (st->halted) return;
+  constexpr int GPB = NT / TG;                    // worker groups per block
   extern __shared__ __align__(16) unsigned char tsm_raw[];
-  TileSmem* sm = reinterpret_cast<TileSmem*>(tsm_raw);
-  __shared__ double sh[TG / 32];
+  const int g = threadIdx.x / TG;
+  TileSmem* sm = reinterpret_cast<TileSmem*>(tsm_raw) + g;
+  __shared__ double sh[NT / 32];
   const int use2 = (MODE == 1) ? st->pending : 1;
   double Wp = 0.0, Yp = 0.0;
-  csr_tiles(blockIdx.x, gridDim.x, threadIdx.x, 0, sm, ptr, idx, val, tiles, ntiles, in1, in2,
-            use2, MODE == 0 ? b : nullptr, o1, o2, Wp, Yp);
+  csr_tiles(blockIdx.x * GPB + g, gridDim.x * GPB, threadIdx.x % TG, 1 + g, sm, ptr, idx, val,
+            tiles, ntiles, in1, in2, use2, MODE == 0 ? b : nullptr, o1, o2, Wp, Yp, nullptr, 0,
+            vec);
   if (MODE == 1) return;
-  const double Wb = block_sum<TG>(Wp, sh);
-  const double Yb = block_sum<TG>(Yp, sh);
+  const double Wb = block_sum<NT>(Wp, sh);
+  const double Yb = block_sum<NT>(Yp, sh);
   if (threadIdx.x == 0) { bpart[blockIdx.x] = Wb; bpart[MAXBLK + blockIdx.x] = Yb; }
   if (!last_block(&st->counters[C_PASSN])) return;
   passN_finish(st, tr, bpart, gridDim.x, sh);

@@ -56,6 +56,7 @@ struct PArgs {
   int ntilesN, ntilesT;
   int greedy;                       // 1 = GDBEK threshold sets instead of sampling
   double eta;
+  int pn_smem;                      // dense pass N: zeta / x staged in shared memory
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -537,6 +538,25 @@ __device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp
   const int rb = (int)((long long)a.m_loc * bb / G), re = (int)((long long)a.m_loc * (bb + 1) / G);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int Q = a.Q, CH = a.CH, n = a.n;
+  // stage the two input vectors in shared memory (LDS instead of L1 loads in
+  // the streaming loop, so the only long-latency loads in flight are A's)
+  const double* v1s = in1;
+  const double* v2s = in2;
+  if (a.pn_smem) {
+    double* zs = np + PN_RB * PN_QMAX * 2;
+    for (int c = threadIdx.x * 2; c < n; c += 2 * PT) {
+      if (c + 1 < n) {
+        *reinterpret_cast<double2*>(zs + c) = *reinterpret_cast<const double2*>(in1 + c);
+        *reinterpret_cast<double2*>(zs + a.lda + c) = *reinterpret_cast<const double2*>(in2 + c);
+      } else {
+        zs[c] = in1[c];
+        zs[a.lda + c] = in2[c];
+      }
+    }
+    __syncthreads();
+    v1s = zs;
+    v2s = zs + a.lda;
+  }
   const int nbatch = (re - rb + PN_RB - 1) / PN_RB;             // evenly sized batches
   const int per = nbatch ? (re - rb + nbatch - 1) / nbatch : 0;
   for (int r0 = rb; r0 < re; r0 += per) {
@@ -551,10 +571,28 @@ __device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp
       const double* a0 = a.A + (long long)(r0 + rr) * a.lda;
       const double* a1 = two ? a0 + a.lda : a0;
       double w0 = 0.0, x0 = 0.0, w1 = 0.0, x1 = 0.0;
-#pragma unroll 4
-      for (int c = c0 + lane * 2; c < c1e; c += 64) {
-        const double2 zc = __ldg(reinterpret_cast<const double2*>(in1 + c));
-        const double2 xc = __ldg(reinterpret_cast<const double2*>(in2 + c));
+      int c = c0 + lane * 2;
+      // batches of 4 column groups: all 8 A loads issued before any use
+      for (; c + 192 < c1e; c += 256) {
+        double2 va[4], vb[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          va[g] = ld_stream2(a0 + c + 64 * g);
+          vb[g] = two ? ld_stream2(a1 + c + 64 * g) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const double2 zc = *reinterpret_cast<const double2*>(v1s + c + 64 * g);
+          const double2 xc = *reinterpret_cast<const double2*>(v2s + c + 64 * g);
+          w0 = fma(va[g].x, zc.x, w0); w0 = fma(va[g].y, zc.y, w0);
+          x0 = fma(va[g].x, xc.x, x0); x0 = fma(va[g].y, xc.y, x0);
+          w1 = fma(vb[g].x, zc.x, w1); w1 = fma(vb[g].y, zc.y, w1);
+          x1 = fma(vb[g].x, xc.x, x1); x1 = fma(vb[g].y, xc.y, x1);
+        }
+      }
+      for (; c < c1e; c += 64) {
+        const double2 zc = *reinterpret_cast<const double2*>(v1s + c);
+        const double2 xc = *reinterpret_cast<const double2*>(v2s + c);
         const double2 v0 = ld_stream2(a0 + c);
         const double2 v1 = two ? ld_stream2(a1 + c) : make_double2(0.0, 0.0);
         w0 = fma(v0.x, zc.x, w0); w0 = fma(v0.y, zc.y, w0);
@@ -790,7 +828,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       const int g = threadIdx.x / TG;
       csr_tiles(blockIdx.x * (PT / TG) + g, G * (PT / TG), threadIdx.x % TG, 1 + g,
                 reinterpret_cast<TileSmem*>(dyn) + g, a.cp, a.ri, a.rv, a.tilesT, a.ntilesT,
-                a.z, a.xi, pending, nullptr, a.s, a.v, Vp, Emax, &ep);
+                a.z, a.xi, pending, nullptr, a.s, a.v, Vp, Emax, &ep, 0, a.vecT);
       __syncthreads();
       flush_hist<PT>(h, hn, NBINS);
       {
@@ -873,7 +911,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
         const int g = threadIdx.x / TG;
         csr_tiles(blockIdx.x * (PT / TG) + g, G * (PT / TG), threadIdx.x % TG, 1 + g,
                   reinterpret_cast<TileSmem*>(dyn) + g, a.rp, a.ci, a.cv, a.tilesN, a.ntilesN,
-                  a.zeta, a.x, 1, a.b, a.w, a.ax, Wp, Yp);
+                  a.zeta, a.x, 1, a.b, a.w, a.ax, Wp, Yp, nullptr, 0, a.vecN);
       }
       const double wb = pblock_sum(Wp, sh);
       const double yb = pblock_sum(Yp, sh);

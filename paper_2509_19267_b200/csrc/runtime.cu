@@ -298,9 +298,11 @@ rgdbek_status build_tiles(rgdbek_ctx* h, const long long* d_ptr, long long rows,
   return RGDBEK_OK;
 }
 
+// Lanes per row in the tile row-sum phase: the largest power of two v with 16 v <= the
+// mean row length, in [1, 32] (measured: C3 5 nnz/row -> 1, C4 41 -> 4 best).
 int pick_vec(double avg) {
-  int v = 2;
-  while (v < 32 && v < avg) v <<= 1;
+  int v = 1;
+  while (v < 32 && 16.0 * (2 * v) <= avg) v <<= 1;
   return v;
 }
 
@@ -340,9 +342,10 @@ void launch_passT(rgdbek_ctx* h) {
     k_dense_passT<PT_TPB><<<grid, PT_TPB, 2 * h->R * sizeof(double), h->stream>>>(
         h->A, h->lda, (int)h->m_loc, (int)h->n, h->R, h->z, h->xi, h->part, h->st);
   } else {
-    k_csr_tiles<1><<<std::min(h->ntilesT, h->tile_grid), TG, sizeof(TileSmem), h->stream>>>(
+    k_csr_tiles<1><<<std::min((h->ntilesT + NT / TG - 1) / (NT / TG), h->tile_grid), NT,
+                     (NT / TG) * sizeof(TileSmem), h->stream>>>(
         h->cp, h->ri, h->rv, h->tilesT, h->ntilesT, h->z, h->xi, nullptr, h->s, h->v, h->st,
-        h->trace, h->bpart);
+        h->trace, h->bpart, h->vecT);
   }
 }
 
@@ -357,9 +360,10 @@ void launch_passN(rgdbek_ctx* h) {
     k_dense_reduceN<<<nblocks(h->m_loc, NT, MAXBLK), NT, 0, h->stream>>>(
         h->npart, h->nQ, (int)h->m_loc, h->b, h->w, h->ax, h->st, h->trace, h->bpart);
   } else {
-    k_csr_tiles<0><<<std::min(h->ntilesN, h->tile_grid), TG, sizeof(TileSmem), h->stream>>>(
+    k_csr_tiles<0><<<std::min((h->ntilesN + NT / TG - 1) / (NT / TG), h->tile_grid), NT,
+                     (NT / TG) * sizeof(TileSmem), h->stream>>>(
         h->rp, h->ci, h->cv, h->tilesN, h->ntilesN, h->zeta, h->x, h->b, h->w, h->ax, h->st,
-        h->trace, h->bpart);
+        h->trace, h->bpart, h->vecN);
   }
 }
 
@@ -543,6 +547,14 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
   h->p_dyn = h->dense ? std::max<size_t>(2 * ZCH * sizeof(double), (size_t)PN_RB * PN_QMAX * 2 * sizeof(double))
                      : (PT / TG) * sizeof(TileSmem);
+  int pn_smem = 0;
+  if (h->dense) {
+    // dense pass N stages zeta and x (2 x lda doubles) after its partials when they fit
+    const size_t need = (size_t)PN_RB * PN_QMAX * 2 * sizeof(double) + 2 * (size_t)h->lda * sizeof(double);
+    // measured on C2c: no gain over L1-cached vectors once A's loads are batched,
+    // so it is opt-in (RGDBEK_PN_SMEM=1)
+    if (need <= 200 * 1024 && getenv("RGDBEK_PN_SMEM")) { h->p_dyn = std::max(h->p_dyn, need); pn_smem = 1; }
+  }
   CK(h, cudaFuncSetAttribute(k_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->p_dyn));
   CK(h, cudaFuncSetAttribute(k_persistent_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->p_dyn));
   CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persistent, PT, h->p_dyn));
@@ -571,7 +583,9 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
   if (h->dense) {
     const long long rows = std::max<long long>(1, std::min<long long>(PN_RB, (h->m_loc + G - 1) / G));
     const long long pairs = (rows + 1) / 2;     // units are 2 rows x 1 chunk
-    long long q = std::max<long long>(1, std::min<long long>(PN_QMAX, (16 * PW + pairs - 1) / pairs));
+    long long units_per_warp = 16;
+    if (const char* e = getenv("RGDBEK_PN_UNITS")) units_per_warp = std::max(1, atoi(e));
+    long long q = std::max<long long>(1, std::min<long long>(PN_QMAX, (units_per_warp * PW + pairs - 1) / pairs));
     long long ch = (h->n + q - 1) / q;
     ch = std::max<long long>(64, (ch + 63) / 64 * 64);
     q = (h->n + ch - 1) / ch;
@@ -591,6 +605,7 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
   a.tilesN = h->tilesN; a.tilesT = h->tilesT; a.ntilesN = h->ntilesN; a.ntilesT = h->ntilesT;
   a.greedy = 0;
   a.eta = h->eta;
+  a.pn_smem = pn_smem;
   if (const char* e = getenv("RGDBEK_PHASE_TIMING")) {
     if (atoi(e)) {
       TRY(dalloc(h, &h->ptime, 16));
@@ -1013,6 +1028,10 @@ rgdbek_status rgdbek_create_csr(rgdbek_handle* out, int64_t m, int64_t n, int64_
   const double avg_c = (double)nnz_local / (double)h->n;
   h->vecN = pick_vec(avg_r);
   h->vecT = pick_vec(avg_c);
+  if (const char* e = getenv("RGDBEK_TILE_VEC")) {       // tuning override (power of two)
+    const int v = atoi(e);
+    if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) h->vecN = h->vecT = v;
+  }
   if ((s = build_tiles(h, h->rp, h->m_loc, &h->tilesN, &h->ntilesN)) != RGDBEK_OK) return create_fail(h, s);
   if (h->cp == h->rp) {
     h->tilesT = h->tilesN; h->ntilesT = h->ntilesN;
@@ -1022,9 +1041,10 @@ rgdbek_status rgdbek_create_csr(rgdbek_handle* out, int64_t m, int64_t n, int64_
   {
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
-    cudaFuncSetAttribute(k_csr_tiles<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem));
-    cudaFuncSetAttribute(k_csr_tiles<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_tiles<0>, TG, sizeof(TileSmem));
+    const int tsm = (int)((NT / TG) * sizeof(TileSmem));
+    cudaFuncSetAttribute(k_csr_tiles<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+    cudaFuncSetAttribute(k_csr_tiles<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_tiles<0>, NT, tsm);
     h->tile_grid = std::max(1, std::min(MAXBLK, nsm * std::max(occ, 1)));
   }
   if ((s = finish_create(h)) != RGDBEK_OK) return create_fail(h, s);
