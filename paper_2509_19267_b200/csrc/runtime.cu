@@ -298,11 +298,11 @@ rgdbek_status build_tiles(rgdbek_ctx* h, const long long* d_ptr, long long rows,
   return RGDBEK_OK;
 }
 
-// Lanes per row in the tile row-sum phase: the largest power of two v with 16 v <= the
+// Lanes per row in the tile row-sum phase: the largest power of two v with 8 v <= the
 // mean row length, in [1, 32] (measured: C3 5 nnz/row -> 1, C4 41 -> 4 best).
 int pick_vec(double avg) {
   int v = 1;
-  while (v < 32 && 16.0 * (2 * v) <= avg) v <<= 1;
+  while (v < 32 && 8.0 * (2 * v) <= avg) v <<= 1;
   return v;
 }
 
