@@ -42,6 +42,7 @@ WORKLOADS = {
     "C3": "2-D Poisson 5-point, 4M unknowns, CSR symmetric (BASELINE configs[2])",
     "C4": "1-D Gaussian Toeplitz blur sigma=r=20 on 1024^2 image + noise (BASELINE configs[3])",
     "C5s": "population-model sliding window 50000x5000, 20 nnz/row, inconsistent (configs[4] scaled)",
+    "C5": "population-model sliding window 50M x 5M, 1e9 nnz, inconsistent (BASELINE configs[4], 1 GPU)",
 }
 
 

@@ -11,7 +11,8 @@ Configs (BASELINE.json "configs", made concrete in SURVEY.md §8(d)):
   C3   2-D Poisson 5-point stencil on a 2000^2 interior grid   (configs[2])
   C4   1-D Gaussian Toeplitz blur sigma=r=20 (eq:toeplitz) on a
        vectorised 1024x1024 image, plus noise                  (configs[3])
-  C5s  population-model sliding-window system 50000x5000       (configs[4], scaled)
+  C5   population-model sliding-window system 50M x 5M, 1e9 nnz (configs[4])
+  C5s  the same generator at 50000x5000                        (configs[4], scaled)
 """
 from dataclasses import dataclass, field
 from typing import Optional
@@ -221,8 +222,13 @@ def popmodel(m, n, seed=0, width=20, noise_frac=0.1, sigma=3.0, delay=1, eta=0.5
     i = np.arange(m, dtype=np.int64)
     c = (i * (n - width)) // max(m - 1, 1)
     t = np.arange(width, dtype=np.int64)
-    cols = (c[:, None] + t[None, :]).ravel().astype(np.int32)
-    vals = sig[(i[:, None] + t[None, :]) % S].ravel()
+    cols = np.empty(m * width, dtype=np.int32)
+    vals = np.empty(m * width, dtype=np.float64)
+    CH = 1 << 20                                     # rows per chunk (bounded temporaries)
+    for r0 in range(0, m, CH):
+        r1 = min(m, r0 + CH)
+        cols[r0 * width:r1 * width] = (c[r0:r1, None] + t[None, :]).ravel()
+        vals[r0 * width:r1 * width] = sig[(i[r0:r1, None] + t[None, :]) % S].ravel()
     indptr = np.arange(0, m * width + 1, width, dtype=np.int64)
     A = sp.csr_matrix((vals, cols, indptr), shape=(m, n))
     x_true = rng.standard_normal(n)
@@ -231,20 +237,25 @@ def popmodel(m, n, seed=0, width=20, noise_frac=0.1, sigma=3.0, delay=1, eta=0.5
     if noise_frac > 0:
         nblk = m // block
         if nblk > 0:
-            rr = i[: nblk * block].reshape(nblk, block)
-            c0 = c[rr[:, 0]]
-            loc = (c[rr][:, :, None] + t[None, None, :]) - c0[:, None, None]
-            Ab = np.zeros((nblk, block, int(loc.max()) + 1))
-            vv = vals.reshape(m, width)[: nblk * block].reshape(nblk, block, width)
-            bi = np.repeat(np.arange(nblk), block * width)
-            ri = np.tile(np.repeat(np.arange(block), width), nblk)
-            Ab[bi, ri, loc.ravel()] = vv.ravel()
-            if Ab.shape[2] >= block:
-                raise ValueError("row blocks too short to have a left null space")
-            U, _, _ = np.linalg.svd(Ab, full_matrices=True)
-            nullv = U[:, :, -1]
             coef = rng.standard_normal(nblk)
-            rvec[: nblk * block] = (coef[:, None] * nullv).ravel()
+            vv_all = vals.reshape(m, width)
+            BCH = 1 << 16                            # blocks per chunk
+            for b0 in range(0, nblk, BCH):
+                b1 = min(nblk, b0 + BCH)
+                nb = b1 - b0
+                rr = i[b0 * block:b1 * block].reshape(nb, block)
+                c0 = c[rr[:, 0]]
+                loc = (c[rr][:, :, None] + t[None, None, :]) - c0[:, None, None]
+                span = int(loc.max()) + 1
+                if span >= block:
+                    raise ValueError("row blocks too short to have a left null space")
+                Ab = np.zeros((nb, block, span))
+                vv = vv_all[b0 * block:b1 * block].reshape(nb, block, width)
+                bi = np.repeat(np.arange(nb), block * width)
+                ri = np.tile(np.repeat(np.arange(block), width), nb)
+                Ab[bi, ri, loc.ravel()] = vv.ravel()
+                U, _, _ = np.linalg.svd(Ab, full_matrices=True)
+                rvec[b0 * block:b1 * block] = (coef[b0:b1, None] * U[:, :, -1]).ravel()
             rvec *= noise_frac * np.linalg.norm(Ax) / np.linalg.norm(rvec)
     b = Ax + rvec
     return Workload(f"popmodel_{m}x{n}", A, b, x_true, rvec, eta=eta,
@@ -278,6 +289,7 @@ CONFIGS = {
     "C3": lambda: poisson2d(2000),
     "C4": lambda: toeplitz_blur(1024 * 1024),
     "C5s": lambda: popmodel(50000, 5000, seed=0),
+    "C5": lambda: popmodel(50_000_000, 5_000_000, seed=0),
     # small twins used by parity tests
     "C2s": lambda: dense_gaussian(2000, 500, seed=0),
     "C2si": lambda: dense_gaussian(2000, 500, seed=0, noise=0.1),
