@@ -57,6 +57,7 @@ struct PArgs {
   int greedy;                       // 1 = GDBEK threshold sets instead of sampling
   double eta;
   int pn_smem;                      // dense pass N: zeta / x staged in shared memory
+  int pt_rows;                      // dense pass T: one-sweep register-column form
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -401,6 +402,81 @@ __device__ void p_sel_level3(PSel* ps, const unsigned int* gh, const Cand* cand,
   __syncthreads();
 }
 
+// Local selection with the level-1 bucket's keys gathered into shared memory
+// once (when they fit): levels 2, 3 and the survivor rank then run on the smem
+// list instead of two more passes over all N keys in global memory.
+constexpr int LCAND_CAP = 4096;
+__device__ bool p_sel_local_smem(PSel* ps, const unsigned long long* __restrict__ keys,
+                                 long long N, long long idx_base, const unsigned int* gh1,
+                                 unsigned int* h, unsigned int* sh_u, long long* sh_l,
+                                 Cand* cl, Cand* fc) {
+  if (ps->mode != SEL_PENDING) return true;
+  const unsigned int c1 = __ldcg(gh1 + ps->prefix);
+  if (c1 > (unsigned int)LCAND_CAP) return false;
+  __shared__ int nc, nf;
+  if (threadIdx.x == 0) { nc = 0; nf = 0; }
+  __syncthreads();
+  const unsigned long long pre1 = ps->prefix;
+  for (long long i = threadIdx.x; i < N; i += PT) {
+    const unsigned long long key = keys[i];
+    if ((key >> L1_SHIFT) == pre1) {
+      const int s = atomicAdd(&nc, 1);
+      if (s < LCAND_CAP) cl[s] = Cand{key, idx_base + i};
+    }
+  }
+  __syncthreads();
+  const int cnt = nc < LCAND_CAP ? nc : LCAND_CAP;
+  for (int lv = 2; lv <= 3; ++lv) {
+    const int sf = lv == 2 ? L1_SHIFT : L2_SHIFT;
+    const int sd = lv == 2 ? L2_SHIFT : L3_SHIFT;
+    for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
+    __syncthreads();
+    const unsigned long long pre = ps->prefix;
+    for (int e = threadIdx.x; e < cnt; e += PT) {
+      const unsigned long long key = cl[e].key;
+      if ((key >> sf) == pre) atomicAdd(&h[(key >> sd) & 0xFFFull], 1u);
+    }
+    __syncthreads();
+    int digit;
+    long long below;
+    p_find_bucket(h, ps->target - ps->below, sh_u, sh_l, digit, below);
+    if (threadIdx.x == 0) {
+      ps->prefix = (ps->prefix << 12) | (unsigned long long)digit;
+      ps->below += below;
+    }
+    __syncthreads();
+  }
+  const unsigned long long pre3 = ps->prefix;
+  for (int e = threadIdx.x; e < cnt; e += PT) {
+    const Cand c = cl[e];
+    if ((c.key >> L3_SHIFT) == pre3) {
+      const int s = atomicAdd(&nf, 1);
+      if (s < FINAL_CAP) fc[s] = c;
+    }
+  }
+  __syncthreads();
+  const int nfin = nf;
+  if (nfin > FINAL_CAP) {
+    __syncthreads();
+    p_sel_slow(ps, keys, N, idx_base, h, sh_u, sh_l);
+    return true;
+  }
+  const long long need = ps->target - ps->below;
+  for (int e = threadIdx.x; e < nfin; e += PT) {
+    const Cand me = fc[e];
+    long long rank = 0;
+    for (int f = 0; f < nfin; ++f) {
+      const Cand o = fc[f];
+      rank += (o.key < me.key) || (o.key == me.key && o.idx < me.idx);
+    }
+    if (rank == need - 1) { ps->tau = me.key; ps->tie = me.idx; }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) ps->mode = SEL_THRESH;
+  __syncthreads();
+  return true;
+}
+
 // Small selections (N <= LOCAL_SEL_MAX): after the grid-wide level-1 bucket,
 // every CTA resolves levels 2, 3 and the survivors by itself from all N keys
 // (identical results everywhere), saving two grid barriers.
@@ -472,13 +548,25 @@ __device__ __forceinline__ bool p_selected(const PSel* ps, unsigned long long ke
 // Dense pass T for this CTA's contiguous row range, all columns (column tiles
 // of 2*PT): part[cta][0][j] = sum_i A_ij z_i, part[cta][1][j] = sum_i A_ij xi_i.
 // ---------------------------------------------------------------------------
+template <int KP>
+__device__ void p_dense_passT_rows(const PArgs& a, int pending, double* zs, const double* in1,
+                                   const double* in2);
+
 __device__ void p_dense_passT(const PArgs& a, int pending, double* zs,
                               const double* in1 = nullptr, const double* in2 = nullptr) {
   if (!in1) in1 = a.z;
   if (!in2) in2 = a.xi;
+  const int ntiles = (a.n + 2 * PT - 1) / (2 * PT);
+  if (a.pt_rows) {
+    switch (ntiles) {
+      case 1: p_dense_passT_rows<1>(a, pending, zs, in1, in2); return;
+      case 2: p_dense_passT_rows<2>(a, pending, zs, in1, in2); return;
+      case 3: p_dense_passT_rows<3>(a, pending, zs, in1, in2); return;
+      default: break;
+    }
+  }
   const int G = gridDim.x, bb = blockIdx.x;
   const int rb = (int)((long long)a.m_loc * bb / G), re = (int)((long long)a.m_loc * (bb + 1) / G);
-  const int ntiles = (a.n + 2 * PT - 1) / (2 * PT);
   double* out = a.part + (long long)bb * 2 * a.n;
   for (int t = 0; t < ntiles; ++t) {
     const int c = t * 2 * PT + 2 * threadIdx.x;
@@ -516,6 +604,62 @@ __device__ void p_dense_passT(const PArgs& a, int pending, double* zs,
     } else if (c < a.n) {
       out[c] = s0;
       out[a.n + c] = v0;
+    }
+  }
+}
+
+// Dense pass T in ONE sweep over the CTA's rows: thread t accumulates the column
+// pairs 2t + 2*PT*k (k < KP) in registers (no per-tile re-staging of z / xi and
+// no sweep with a partly idle block).
+template <int KP>
+__device__ void p_dense_passT_rows(const PArgs& a, int pending, double* zs, const double* in1,
+                                   const double* in2) {
+  const int G = gridDim.x, bb = blockIdx.x;
+  const int rb = (int)((long long)a.m_loc * bb / G), re = (int)((long long)a.m_loc * (bb + 1) / G);
+  const int n = a.n;
+  double* out = a.part + (long long)bb * 2 * n;
+  double acc[KP][4];
+#pragma unroll
+  for (int k = 0; k < KP; ++k) { acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0; }
+  for (int rc = rb; rc < re; rc += ZCH) {
+    const int rows = min(ZCH, re - rc);
+    __syncthreads();
+    for (int i = threadIdx.x; i < rows; i += PT) {
+      zs[i] = in1[rc + i];
+      zs[ZCH + i] = pending ? in2[rc + i] : 0.0;
+    }
+    __syncthreads();
+    const double* p = a.A + (long long)rc * a.lda + 2 * threadIdx.x;
+#pragma unroll 2
+    for (int i = 0; i < rows; ++i) {
+      const double zi = zs[i], xv = zs[ZCH + i];
+      const double* pr = p + (long long)i * a.lda;
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        const int c = 2 * threadIdx.x + 2 * PT * k;
+        if (c + 1 < n) {
+          const double2 av = ld_stream2(pr + 2 * PT * k);
+          acc[k][0] = fma(av.x, zi, acc[k][0]);
+          acc[k][1] = fma(av.y, zi, acc[k][1]);
+          acc[k][2] = fma(av.x, xv, acc[k][2]);
+          acc[k][3] = fma(av.y, xv, acc[k][3]);
+        } else if (c < n) {
+          const double av = ld_stream(pr + 2 * PT * k);
+          acc[k][0] = fma(av, zi, acc[k][0]);
+          acc[k][2] = fma(av, xv, acc[k][2]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    const int c = 2 * threadIdx.x + 2 * PT * k;
+    if (c + 1 < n) {
+      out[c] = acc[k][0]; out[c + 1] = acc[k][1];
+      out[n + c] = acc[k][2]; out[n + c + 1] = acc[k][3];
+    } else if (c < n) {
+      out[c] = acc[k][0];
+      out[n + c] = acc[k][2];
     }
   }
 }
@@ -852,7 +996,9 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       p_sel_greedy(&ps, slot_max(bp, SL_MAXN, sh), a.eta);
     } else if (n <= LOCAL_SEL_MAX) {
       p_sel_level1(&ps, hn, n, kc, sh_u, sh_l);
-      p_sel_local(&ps, a.keys_n, n, 0, h, sh_u, sh_l);
+      if (!p_sel_local_smem(&ps, a.keys_n, n, 0, hn, h, sh_u, sh_l, reinterpret_cast<Cand*>(dyn),
+                            reinterpret_cast<Cand*>(dyn) + LCAND_CAP))
+        p_sel_local(&ps, a.keys_n, n, 0, h, sh_u, sh_l);
     } else {
       p_sel_level1(&ps, hn, n, kc, sh_u, sh_l);
       p_sel_scan<2>(&ps, a.keys_n, n, 0, hn + NBINS, cn, a.ncand, h);
@@ -983,7 +1129,9 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       p_sel_greedy(&ps, slot_max(bp, SL_MAXM, sh), a.eta);
     } else if (m_loc <= LOCAL_SEL_MAX) {
       p_sel_level1(&ps, hm, m_loc, kr, sh_u, sh_l);
-      p_sel_local(&ps, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
+      if (!p_sel_local_smem(&ps, a.keys_m, m_loc, a.row0, hm, h, sh_u, sh_l,
+                            reinterpret_cast<Cand*>(dyn), reinterpret_cast<Cand*>(dyn) + LCAND_CAP))
+        p_sel_local(&ps, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
     } else {
       p_sel_level1(&ps, hm, m_loc, kr, sh_u, sh_l);
       p_sel_scan<2>(&ps, a.keys_m, m_loc, a.row0, hm + NBINS, cm, a.ncand + 1, h);

@@ -547,6 +547,8 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
   h->p_dyn = h->dense ? std::max<size_t>(2 * ZCH * sizeof(double), (size_t)PN_RB * PN_QMAX * 2 * sizeof(double))
                      : (PT / TG) * sizeof(TileSmem);
+  // local selections gather the level-1 bucket into (LCAND_CAP + FINAL_CAP) Cand of smem
+  h->p_dyn = std::max(h->p_dyn, (size_t)(LCAND_CAP + FINAL_CAP) * sizeof(Cand));
   int pn_smem = 0;
   if (h->dense) {
     // dense pass N stages zeta and x (2 x lda doubles) after its partials when they fit
@@ -606,6 +608,8 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
   a.greedy = 0;
   a.eta = h->eta;
   a.pn_smem = pn_smem;
+  // one-sweep register-column pass T measured slower (223 vs 129 us on C2c): opt-in
+  a.pt_rows = getenv("RGDBEK_PT_ROWS") ? 1 : 0;
   if (const char* e = getenv("RGDBEK_PHASE_TIMING")) {
     if (atoi(e)) {
       TRY(dalloc(h, &h->ptime, 16));
