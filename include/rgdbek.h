@@ -188,15 +188,19 @@ rgdbek_status rgdbek_set_state(rgdbek_handle h, const double* x, const double* z
 rgdbek_status rgdbek_launch_kernel(rgdbek_handle h, int32_t kernel, int32_t reps,
                                    double* bytes_per_launch);
 
-/* Kernels launched per iteration body (for the bench's gpu_launches count). */
+/* Kernels launched per iteration body of the graph engine (for the bench's gpu_launches
+ * count); 0 for the persistent engine, which is one launch per rgdbek_step/solve call. */
 rgdbek_status rgdbek_launches_per_iteration(rgdbek_handle h, int64_t* out);
 
 /* Diagnostics.  rgdbek_phase_times: accumulated device time (ns, %globaltimer read by CTA 0
- * after each grid barrier) of the persistent engine's phases 0..15, when the handle was
- * created with RGDBEK_PHASE_TIMING=1 in the environment; *n_out = 0 otherwise.
+ * after each grid barrier) of the persistent engine's phases, when the handle was
+ * created with RGDBEK_PHASE_TIMING=1 in the environment; *n_out = 0 otherwise.  Up to 24
+ * entries: ids 0..15 are times, 16..17 event counts.
  * Phase ids: 1 pass T, 2 s/v + column keys, 3-4 column selection levels, 5 mask + x update,
  * 6 pass N, 7 stop test + z update + row keys, 8-9 row selection levels, 10 row mask,
- * 0 bookkeeping.  rgdbek_engine_info: engine 0 = persistent kernel (ctas = its grid),
+ * 0 bookkeeping, 11-12 dense column sums / flush, 13-14 local column selection (level 1,
+ * levels 2-3 + rank), 15 local row selection; 16 / 17 = number of local column / row
+ * selections that overflowed the shared-memory candidate list.  rgdbek_engine_info: engine 0 = persistent kernel (ctas = its grid),
  * 1 = multi-kernel CUDA graph (RGDBEK_ENGINE=graph). */
 rgdbek_status rgdbek_phase_times(rgdbek_handle h, double* out_ns, int32_t max_phases,
                                  int32_t* n_out);

@@ -213,9 +213,9 @@ def rgdbek_stream(h):
 
 
 def rgdbek_phase_times(h):
-    buf = (C.c_double * 16)()
+    buf = (C.c_double * 24)()
     cnt = C.c_int32()
-    check(load().rgdbek_phase_times(h, buf, 16, C.byref(cnt)), h)
+    check(load().rgdbek_phase_times(h, buf, 24, C.byref(cnt)), h)
     return [buf[i] for i in range(cnt.value)]
 
 

@@ -1,37 +1,113 @@
-// csr_tiles.cuh — CSR (or CSC) dual SpMV by nnz tiles ("CSR-stream").
+// csr_tiles.cuh — CSR (or CSC) dual SpMV by nnz tiles, fed by TMA bulk copies.
 //
 // A sparse pass computes o1 = A in1 and o2 = A in2 over rows (pass N: A zeta,
-// A x; pass T over the CSC: A^T z, A^T xi).  Short rows (5-41 nnz here) make
-// a row-per-thread or sub-warp-per-row loop a chain of three dependent memory
-// round trips per row (row pointer -> value/index -> gathered vector), so
-// each warp keeps almost nothing in flight.  Instead a worker group of TG
-// threads takes a tile of consecutive rows holding <= TILE_NNZ nonzeros:
-//   1. stage the tile's row pointers in shared memory;
-//   2. stream its values and indices with fully coalesced loads (every thread
-//      ~8 independent loads in flight) and store the products val*in1[idx],
-//      val*in2[idx] in shared memory;
-//   3. sum each row's products in order (deterministic) from shared memory.
-// A row longer than TILE_NNZ is a tile by itself, reduced across the group.
-// Tiles are precomputed at create (greedy on the row pointer).
+// A x; pass T over the CSC: A^T z, A^T xi).  Rows are short (5-41 nnz in the
+// paper's workloads), so a row-per-thread loop is a chain of three dependent
+// memory round trips per row (row pointer -> value/index -> gathered vector)
+// and keeps almost nothing in flight.  Instead a worker group of TG threads
+// takes tiles of consecutive rows holding <= TILE_NNZ nonzeros (precomputed at
+// create, with each tile's first nonzero offset), and:
+//   * one thread of the group streams the tile's row pointers, values and
+//     column indices into shared memory with cp.async.bulk (TMA bulk copies,
+//     completion on an mbarrier), TBUF tiles ahead of the group, so the
+//     matrix stream is always in flight while the group works;
+//   * the group sums each row from shared memory, `vec` lanes per row, with
+//     the gathers in1[c], in2[c] issued four entries at a time; partial sums
+//     are combined by a fixed shuffle tree (deterministic).
+// A row longer than TILE_NNZ is a tile by itself, read straight from global
+// memory and reduced across the group.
 #pragma once
 #include "common.cuh"
 
 namespace rg {
 
 constexpr int TG = 128;              // threads per worker group
-constexpr int TILE_NNZ = 1024;       // 8 nonzeros per thread, in two sub-rounds of 4
-constexpr int TILE_ROWS = 256;
+constexpr int TILE_NNZ = 512;        // nonzeros per tile
+constexpr int TILE_ROWS = 128;       // rows per tile
+constexpr int TBUF = 3;              // tiles in flight per group
 
-struct TileSmem {
-  double p1[TILE_NNZ];
-  double p2[TILE_NNZ];
-  long long rp[TILE_ROWS + 1];
+// One staged tile.  Windows are widened to 16-byte boundaries (bulk-copy
+// alignment): val from p0 & ~1, idx from p0 & ~3, rp from r0 & ~1.
+struct __align__(16) TileBuf {
+  double val[TILE_NNZ + 2];
+  int idx[TILE_NNZ + 8];
+  long long rp[TILE_ROWS + 4];
+};
+static_assert(sizeof(TileBuf) % 16 == 0, "TileBuf must keep 16-byte alignment");
+
+// Pass-T column results waiting for the key epilogue (batched so a tile of a
+// few long columns does not run the ALU-heavy key chain on a few threads).
+struct TilePend {
+  double s1[TG], s2[TG];
+  int row[TG];
+};
+
+struct __align__(16) TileSmem {
+  TileBuf buf[TBUF];
+  long long desc[TBUF][4];       // r0, r1, p0, p1 of the staged tile (written by the producer)
   double red[2 * (TG / 32)];
+  TilePend pend;
 };
 
 // Barrier over this worker group's TG threads (named barrier id >= 1).
 __device__ __forceinline__ void group_bar(int id) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(TG) : "memory");
+}
+
+// Per-group ring state: TBUF "full" mbarriers (in static shared memory, so
+// other phases may reuse the TileSmem area as scratch) and the number of
+// tiles this group has consumed so far (identical in all its threads).
+struct TileRing {
+  unsigned long long* full;   // [TBUF]
+  unsigned int used;
+};
+
+// Initialise a group's barriers (one thread), before the first csr_tiles call;
+// the caller follows with fence.mbarrier_init + a CTA barrier.
+__device__ __forceinline__ void tile_ring_init(unsigned long long* full) {
+  for (int i = 0; i < TBUF; ++i) mbar_init(&full[i], 1);
+}
+
+// CTA prologue of a kernel running csr_tiles: every group's barriers, made
+// visible to the async proxy and to the whole CTA.
+__device__ __forceinline__ void tile_rings_init(unsigned long long* bars) {
+  if (threadIdx.x % TG == 0) tile_ring_init(bars + (threadIdx.x / TG) * TBUF);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+}
+
+// Tile descriptor: rows [r0, r1), nonzeros [p0, p1).
+struct TileDesc {
+  long long r0, r1, p0, p1;
+};
+
+__device__ __forceinline__ TileDesc tile_desc(int t, const int* __restrict__ tiles,
+                                              const long long* __restrict__ tilep) {
+  return TileDesc{__ldg(tiles + t), __ldg(tiles + t + 1), __ldg(tilep + t), __ldg(tilep + t + 1)};
+}
+
+// Issue the bulk copies of tile d into buffer b (one thread).  The descriptor
+// goes to shared memory before the barrier's arrive (release), so consumers
+// read it after their wait (acquire).  Bytes are counted on the barrier
+// before the copies start (arrive.expect_tx).
+__device__ __forceinline__ void tile_issue(TileSmem* sm, int b, unsigned long long* bar,
+                                           const TileDesc& d, const long long* ptr,
+                                           const int* idx, const double* val) {
+  TileBuf* B = &sm->buf[b];
+  sm->desc[b][0] = d.r0; sm->desc[b][1] = d.r1; sm->desc[b][2] = d.p0; sm->desc[b][3] = d.p1;
+  const long long rs = d.r0 & ~1LL, re = (d.r1 + 2) & ~1LL;     // covers rp[r0..r1]
+  const unsigned rb = (unsigned)((re - rs) * sizeof(long long));
+  const bool stage = d.p1 > d.p0 && d.p1 - d.p0 <= TILE_NNZ;
+  const long long vs = d.p0 & ~1LL, ve = (d.p1 + 1) & ~1LL;
+  const long long is = d.p0 & ~3LL, ie = (d.p1 + 3) & ~3LL;
+  const unsigned vb = stage ? (unsigned)((ve - vs) * sizeof(double)) : 0u;
+  const unsigned ib = stage ? (unsigned)((ie - is) * sizeof(int)) : 0u;
+  mbar_expect_tx(bar, rb + vb + ib);
+  bulk_g2s(B->rp, ptr + rs, rb, bar);
+  if (stage) {
+    bulk_g2s(B->val, val + vs, vb, bar);
+    bulk_g2s(B->idx, idx + is, ib, bar);
+  }
 }
 
 // Optional fused epilogue of pass T (persistent engine): column scores
@@ -49,9 +125,8 @@ struct ColKeyEpi {
 };
 
 __device__ __forceinline__ void colkey_epilogue(const ColKeyEpi* ep, int j, double sj, double vj,
-                                                double& Vp, double& Emax) {
+                                                double& Vp, double& Emax, double g) {
   if (ep->pending) Vp += vj * vj;
-  const double g = ep->gamma[j];
   const double eps = g > 0.0 ? __ddiv_rn(__dmul_rn(sj, sj), g) : 0.0;
   Emax = fmax(Emax, eps);
   const unsigned long long key = sel_key(eps, (unsigned long long)j, ep->k, 0u, ep->seed, ep->greedy);
@@ -59,109 +134,152 @@ __device__ __forceinline__ void colkey_epilogue(const ColKeyEpi* ep, int j, doub
   atomicAdd(&ep->hist[key >> L1_SHIFT], 1u);
 }
 
-__device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm,
+// Row results of pass N / the exact mode: outputs and the W / ||b - A x||^2
+// (or ||o1||^2) partials; bv = b[row] loaded ahead by the caller.
+__device__ __forceinline__ void tile_row_out(int row, double s1, double s2, bool has_b, double bv,
+                                             double* o1, double* o2, double& Wp, double& Yp,
+                                             int acc1) {
+  o1[row] = s1;
+  o2[row] = s2;
+  if (has_b) {
+    const double y = bv - s2;
+    Wp += s1 * s1;
+    Yp += y * y;
+  }
+  if (acc1) Wp += s1 * s1;
+}
+
+// Key epilogue of the pending pass-T columns (thread lt takes entry lt).
+__device__ __forceinline__ void tile_flush(const ColKeyEpi* ep, TilePend* pd, int npend, int lt,
+                                           double& Vp, double& Emax) {
+  if (lt < npend) {
+    const int j = pd->row[lt];
+    colkey_epilogue(ep, j, pd->s1[lt], pd->s2[lt], Vp, Emax, ep->gamma[j]);
+  }
+}
+
+__device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm, TileRing& ring,
                           const long long* __restrict__ ptr, const int* __restrict__ idx,
                           const double* __restrict__ val, const int* __restrict__ tiles,
-                          int ntiles, const double* __restrict__ in1,
-                          const double* __restrict__ in2, int use2,
-                          const double* __restrict__ b, double* __restrict__ o1,
-                          double* __restrict__ o2, double& Wp, double& Yp,
+                          const long long* __restrict__ tilep, int ntiles,
+                          const double* in1, const double* in2, int use2,
+                          const double* __restrict__ b, double* o1, double* o2,
+                          double& Wp, double& Yp,
                           const ColKeyEpi* ep = nullptr, int acc1 = 0, int vec = 1) {
-  for (int t = gid; t < ntiles; t += ngroups) {
-    const int r0 = tiles[t], r1 = tiles[t + 1];
-    const int nr = r1 - r0;
-    for (int i = lt; i <= nr; i += TG) sm->rp[i] = ptr[r0 + i];
-    group_bar(bar_id);
-    const long long p0 = sm->rp[0], p1 = sm->rp[nr];
+  const int cnt = gid < ntiles ? (ntiles - gid + ngroups - 1) / ngroups : 0;
+  // the staging buffers may have been scratch of another phase (generic-proxy
+  // writes): order those before the async-proxy (TMA) writes below
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  group_bar(bar_id);
+  if (lt == 0) {
+    for (int i = 0; i < cnt && i < TBUF; ++i) {
+      const unsigned u = ring.used + i;
+      tile_issue(sm, u % TBUF, &ring.full[u % TBUF], tile_desc(gid + i * ngroups, tiles, tilep),
+                 ptr, idx, val);
+    }
+  }
+  const int lane = lt & 31, lw = lt >> 5;
+  const bool has_b = b != nullptr;
+  int npend = 0;                                   // pass T: columns awaiting their keys
+  for (int i = 0; i < cnt; ++i) {
+    const int t = gid + i * ngroups;
+    const unsigned u = ring.used + i, bi = u % TBUF;
+    // the producer fetches the descriptor of the tile it refills this buffer with
+    TileDesc nd{0, 0, 0, 0};
+    const bool refill = lt == 0 && i + TBUF < cnt;
+    if (refill) nd = tile_desc(t + TBUF * ngroups, tiles, tilep);
+    mbar_wait(&ring.full[bi], (u / TBUF) & 1u);
+    const int r0 = (int)sm->desc[bi][0], nr = (int)(sm->desc[bi][1] - sm->desc[bi][0]);
+    const long long p0 = sm->desc[bi][2], p1 = sm->desc[bi][3];
+    if (ep && npend + nr > TG) {                   // make room in the pending list
+      tile_flush(ep, &sm->pend, npend, lt, Wp, Yp);
+      npend = 0;
+      group_bar(bar_id);
+    }
     if (p1 - p0 > TILE_NNZ) {                      // one long row: group-wide reduction
       double a1 = 0.0, a2 = 0.0;
+      const double bv = has_b && lt == 0 ? b[r0] : 0.0;
       for (long long p = p0 + lt; p < p1; p += TG) {
         const double a = ld_stream(val + p);
         const int c = __ldg(idx + p);
-        a1 = fma(a, __ldg(in1 + c), a1);
-        if (use2) a2 = fma(a, __ldg(in2 + c), a2);
+        a1 = fma(a, ld_weak(in1 + c), a1);
+        if (use2) a2 = fma(a, ld_weak(in2 + c), a2);
       }
       a1 = warp_sum(a1);
       a2 = warp_sum(a2);
-      if ((lt & 31) == 0) { sm->red[2 * (lt >> 5)] = a1; sm->red[2 * (lt >> 5) + 1] = a2; }
+      if (lane == 0) { sm->red[2 * lw] = a1; sm->red[2 * lw + 1] = a2; }
       group_bar(bar_id);
       if (lt == 0) {
         double s1 = 0.0, s2 = 0.0;
         for (int q = 0; q < TG / 32; ++q) { s1 += sm->red[2 * q]; s2 += sm->red[2 * q + 1]; }
-        o1[r0] = s1;
-        o2[r0] = s2;
-        if (b) {
-          const double y = b[r0] - s2;
-          Wp += s1 * s1;
-          Yp += y * y;
-        }
-        if (ep) colkey_epilogue(ep, r0, s1, s2, Wp, Yp);
-        if (acc1) Wp += s1 * s1;
-      }
-      group_bar(bar_id);
-      continue;
-    }
-    const int nz = (int)(p1 - p0);
-    // sub-rounds of SUB entries per thread, each in two phases (all values /
-    // indices first, then all gathers), so SUB independent chains are in flight
-    constexpr int SUB = 4;
-    for (int e0 = 0; e0 < TILE_NNZ / TG; e0 += SUB) {
-      double av[SUB], g1[SUB], g2[SUB];
-      int ci[SUB];
-#pragma unroll
-      for (int e = 0; e < SUB; ++e) {
-        const int q = lt + (e0 + e) * TG;
-        av[e] = 0.0; ci[e] = 0;
-        if (q < nz) { av[e] = ld_stream(val + p0 + q); ci[e] = __ldg(idx + p0 + q); }
-      }
-#pragma unroll
-      for (int e = 0; e < SUB; ++e) {
-        const int q = lt + (e0 + e) * TG;
-        g1[e] = 0.0; g2[e] = 0.0;
-        if (q < nz) {
-          g1[e] = __ldg(in1 + ci[e]);
-          if (use2) g2[e] = __ldg(in2 + ci[e]);
+        if (ep) {
+          o1[r0] = s1;
+          o2[r0] = s2;
+          sm->pend.s1[npend] = s1; sm->pend.s2[npend] = s2; sm->pend.row[npend] = r0;
+        } else {
+          tile_row_out(r0, s1, s2, has_b, bv, o1, o2, Wp, Yp, acc1);
         }
       }
+    } else {
+      // lanes per row for this tile: the mean-length choice `vec`, raised so the
+      // tile's rows cover the whole group (a tile of few long rows still keeps
+      // every thread busy); a power of two <= 32, uniform across the tile
+      int v = vec;
+      while (v < 32 && nr * (2 * v) <= TG) v <<= 1;
+      const int spw = 32 / v, sub = lane / v, sl = lane & (v - 1);
+      const TileBuf& B = sm->buf[bi];
+      const long long* R = B.rp + (r0 & 1);        // R[r] = ptr[r0 + r]
+      const double* V = B.val + (p0 & 1);          // V[q] = val[p0 + q]
+      const int* I = B.idx + (p0 & 3);             // I[q] = idx[p0 + q]
+      for (int base = lw * spw; base < nr; base += (TG / 32) * spw) {   // warp-uniform bounds
+        const int r = base + sub;
+        const bool valid = r < nr;
+        double s1 = 0.0, s2 = 0.0;
+        const double bv = has_b && valid && sl == 0 ? b[r0 + r] : 0.0;   // ahead of the gathers
+        if (valid) {
+          int q = (int)(R[r] - p0) + sl;
+          const int q1 = (int)(R[r + 1] - p0);
+          for (; q + 3 * v < q1; q += 4 * v) {       // four entries: gathers in flight together
+            double a[4], g1[4], g2[4];
 #pragma unroll
-      for (int e = 0; e < SUB; ++e) {
-        const int q = lt + (e0 + e) * TG;
-        if (q < nz) { sm->p1[q] = av[e] * g1[e]; sm->p2[q] = av[e] * g2[e]; }
-      }
-      if (lt + (e0 + SUB) * TG >= nz) break;
-    }
-    group_bar(bar_id);
-    // row sums: vec lanes per row (power of two, chosen from the mean row length),
-    // strided partial sums then a fixed shuffle tree — deterministic; loop
-    // bounds are warp-uniform so the shuffles are well defined
-    const int lane = lt & 31, lw = lt >> 5;
-    const int spw = 32 / vec, sub = lane / vec, sl = lane & (vec - 1);
-    for (int base = lw * spw; base < nr; base += (TG / 32) * spw) {
-      const int r = base + sub;
-      const bool valid = r < nr;
-      double s1 = 0.0, s2 = 0.0;
-      if (valid) {
-        const int q0 = (int)(sm->rp[r] - p0), q1 = (int)(sm->rp[r + 1] - p0);
-        for (int q = q0 + sl; q < q1; q += vec) { s1 += sm->p1[q]; s2 += sm->p2[q]; }
-      }
-      for (int o = vec >> 1; o > 0; o >>= 1) {
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o, vec);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, o, vec);
-      }
-      if (valid && sl == 0) {
-        o1[r0 + r] = s1;
-        o2[r0 + r] = s2;
-        if (b) {
-          const double y = b[r0 + r] - s2;
-          Wp += s1 * s1;
-          Yp += y * y;
+            for (int e = 0; e < 4; ++e) a[e] = V[q + e * v];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int c = I[q + e * v];
+              g1[e] = ld_weak(in1 + c);
+              g2[e] = use2 ? ld_weak(in2 + c) : 0.0;
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) { s1 = fma(a[e], g1[e], s1); s2 = fma(a[e], g2[e], s2); }
+          }
+          for (; q < q1; q += v) {
+            const double a = V[q];
+            const int c = I[q];
+            s1 = fma(a, ld_weak(in1 + c), s1);
+            if (use2) s2 = fma(a, ld_weak(in2 + c), s2);
+          }
         }
-        if (ep) colkey_epilogue(ep, r0 + r, s1, s2, Wp, Yp);
-        if (acc1) Wp += s1 * s1;
+        for (int o = v >> 1; o > 0; o >>= 1) {
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o, v);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, o, v);
+        }
+        if (valid && sl == 0) {
+          if (ep) {
+            o1[r0 + r] = s1;
+            o2[r0 + r] = s2;
+            sm->pend.s1[npend + r] = s1; sm->pend.s2[npend + r] = s2; sm->pend.row[npend + r] = r0 + r;
+          } else {
+            tile_row_out(r0 + r, s1, s2, has_b, bv, o1, o2, Wp, Yp, acc1);
+          }
+        }
       }
     }
-    group_bar(bar_id);
+    npend += nr;
+    group_bar(bar_id);                              // buffer bi free again; pend entries visible
+    if (refill) tile_issue(sm, bi, &ring.full[bi], nd, ptr, idx, val);
   }
+  if (ep) tile_flush(ep, &sm->pend, npend, lt, Wp, Yp);
+  ring.used += cnt;
 }
 
 }  // namespace rg

@@ -249,9 +249,9 @@ template <int MODE>
 __global__ void __launch_bounds__(NT) k_csr_tiles(const long long* __restrict__ ptr,
                                                  const int* __restrict__ idx,
                                                  const double* __restrict__ val,
-                                                 const int* __restrict__ tiles, int ntiles,
-                                                 const double* __restrict__ in1,
-                                                 const double* __restrict__ in2,
+                                                 const int* __restrict__ tiles,
+                                                 const long long* __restrict__ tilep, int ntiles,
+                                                 const double* in1, const double* in2,
                                                  const double* __restrict__ b,
                                                  double* __restrict__ o1, double* __restrict__ o2,
                                                  Scal* st, TraceRec* tr, double* bpart,
@@ -262,11 +262,14 @@ __global__ void __launch_bounds__(NT) k_csr_tiles(const long long* __restrict__ 
   const int g = threadIdx.x / TG;
   TileSmem* sm = reinterpret_cast<TileSmem*>(tsm_raw) + g;
   __shared__ double sh[NT / 32];
+  __shared__ __align__(8) unsigned long long tbar[GPB * TBUF];
+  tile_rings_init(tbar);
+  TileRing ring{tbar + g * TBUF, 0u};
   const int use2 = (MODE == 1) ? st->pending : 1;
   double Wp = 0.0, Yp = 0.0;
-  csr_tiles(blockIdx.x * GPB + g, gridDim.x * GPB, threadIdx.x % TG, 1 + g, sm, ptr, idx, val,
-            tiles, ntiles, in1, in2, use2, MODE == 0 ? b : nullptr, o1, o2, Wp, Yp, nullptr, 0,
-            vec);
+  csr_tiles(blockIdx.x * GPB + g, gridDim.x * GPB, threadIdx.x % TG, 1 + g, sm, ring, ptr, idx,
+            val, tiles, tilep, ntiles, in1, in2, use2, MODE == 0 ? b : nullptr, o1, o2, Wp, Yp,
+            nullptr, 0, vec);
   if (MODE == 1) return;
   const double Wb = block_sum<NT>(Wp, sh);
   const double Yb = block_sum<NT>(Yp, sh);

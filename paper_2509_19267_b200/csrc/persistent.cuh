@@ -53,11 +53,13 @@ struct PArgs {
   GridBar* bar;
   unsigned long long* ptime;        // optional per-phase device time (ns), [16]
   const int* tilesN; const int* tilesT;
+  const long long* tilepN; const long long* tilepT;   // first nonzero of each tile
   int ntilesN, ntilesT;
   int greedy;                       // 1 = GDBEK threshold sets instead of sampling
   double eta;
   int pn_smem;                      // dense pass N: zeta / x staged in shared memory
   int pt_rows;                      // dense pass T: one-sweep register-column form
+  int pn_tma;                       // dense pass N: TMA ring stages (0 = off)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -245,13 +247,23 @@ __device__ void p_sel_scan(const PSel* ps, const unsigned long long* __restrict_
   constexpr int SD = (LEVEL == 2) ? L2_SHIFT : L3_SHIFT;
   const unsigned long long pre = ps->prefix;
   const long long stride = (long long)gridDim.x * PT;
-  for (long long i = (long long)blockIdx.x * PT + threadIdx.x; i < N; i += stride) {
-    const unsigned long long key = keys[i];
-    if ((key >> SF) == pre) {
-      atomicAdd(&h[(key >> SD) & 0xFFFull], 1u);
-      if (LEVEL == 3) {
-        const unsigned int slot = atomicAdd(ncand, 1u);
-        if (slot < CAND_CAP) cand[slot] = Cand{key, idx_base + i};
+  constexpr int VU = 4;                         // keys in flight per thread
+  for (long long i0 = (long long)blockIdx.x * PT + threadIdx.x; i0 < N; i0 += VU * stride) {
+    unsigned long long kv[VU];
+#pragma unroll
+    for (int e = 0; e < VU; ++e) {
+      const long long i = i0 + e * stride;
+      kv[e] = i < N ? keys[i] : KEY_NEVER;
+    }
+#pragma unroll
+    for (int e = 0; e < VU; ++e) {
+      const unsigned long long key = kv[e];
+      if (i0 + e * stride < N && (key >> SF) == pre) {
+        atomicAdd(&h[(key >> SD) & 0xFFFull], 1u);
+        if (LEVEL == 3) {
+          const unsigned int slot = atomicAdd(ncand, 1u);
+          if (slot < CAND_CAP) cand[slot] = Cand{key, idx_base + i0 + e * stride};
+        }
       }
     }
   }
@@ -669,6 +681,100 @@ __device__ void p_dense_passT_rows(const PArgs& a, int pending, double* zs, cons
 // (1 row) x (column chunk of CH), partials in smem, summed in chunk order.
 // Returns this thread's contributions to W and ||b - Ax||^2.
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Dense pass N with a TMA bulk-copy pipeline (RGDBEK_PN_TMA=1): warp 0 lane 0
+// streams the CTA's rows of A into a ring of S shared-memory stages with
+// cp.async.bulk (completion on an mbarrier, expect_tx), so the HBM stream never
+// waits for the math; warps 1..31 own fixed column pairs with zeta / x in
+// registers, read each row from shared memory, reduce per warp with shuffles,
+// release the stage, and every 32 rows add the 31 warp partials of each row in
+// warp order (deterministic).  Ring state persists across calls (u_prod, u_cons).
+// ---------------------------------------------------------------------------
+constexpr int TMA_STAGES_MAX = 8;
+struct TmaRing {
+  unsigned long long full[TMA_STAGES_MAX];
+  unsigned long long empty[TMA_STAGES_MAX];
+};
+
+template <int KP>
+__device__ void p_dense_passN_tma(const PArgs& a, double* dyn, TmaRing* ring, int S,
+                                  long long& u_ring, double& Wp, double& Yp) {
+  const int G = gridDim.x, bb = blockIdx.x;
+  const int rb = (int)((long long)a.m_loc * bb / G), re = (int)((long long)a.m_loc * (bb + 1) / G);
+  const int n = a.n;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned rowbytes = (unsigned)(a.lda * sizeof(double));
+  double* stage0 = dyn;                                           // S x lda doubles
+  double* red = dyn + (long long)S * a.lda;                       // [32 rows][31 warps][2]
+  constexpr int NCW = PW - 1;                                     // consumer warps
+  if (wid == 0) {
+    // ---- producer ----
+    if (lane == 0) {
+      for (int i = rb; i < re; ++i) {
+        const long long u = u_ring + (i - rb);
+        const int st = (int)(u % S);
+        if (u >= S) mbar_wait(&ring->empty[st], (unsigned)(((u / S) - 1) & 1));
+        mbar_expect_tx(&ring->full[st], rowbytes);
+        bulk_g2s(stage0 + (long long)st * a.lda, a.A + (long long)i * a.lda, rowbytes, &ring->full[st]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---- consumers ----
+    const int ct = threadIdx.x - 32;                              // 0 .. 991
+    double2 zr[KP], xr[KP];
+    bool ok[KP];
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      const int c = 2 * ct + 2 * 32 * NCW * k;
+      ok[k] = c + 1 < n;
+      zr[k] = ok[k] ? *reinterpret_cast<const double2*>(a.zeta + c) : make_double2(0.0, 0.0);
+      xr[k] = ok[k] ? *reinterpret_cast<const double2*>(a.x + c) : make_double2(0.0, 0.0);
+    }
+    const bool odd = (n & 1) && ct == 0;
+    const double zl = odd ? a.zeta[n - 1] : 0.0, xl = odd ? a.x[n - 1] : 0.0;
+    for (int r0 = rb; r0 < re; r0 += 32) {
+      const int rows = min(32, re - r0);
+      for (int rr = 0; rr < rows; ++rr) {
+        const long long u = u_ring + (r0 + rr - rb);
+        const int st = (int)(u % S);
+        mbar_wait(&ring->full[st], (unsigned)((u / S) & 1));
+        const double* row = stage0 + (long long)st * a.lda;
+        double sw = 0.0, sx = 0.0;
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          if (ok[k]) {
+            const double2 v = *reinterpret_cast<const double2*>(row + 2 * ct + 2 * 32 * NCW * k);
+            sw = fma(v.x, zr[k].x, sw); sw = fma(v.y, zr[k].y, sw);
+            sx = fma(v.x, xr[k].x, sx); sx = fma(v.y, xr[k].y, sx);
+          }
+        }
+        if (odd) { const double v = row[n - 1]; sw = fma(v, zl, sw); sx = fma(v, xl, sx); }
+        sw = warp_sum(sw);
+        sx = warp_sum(sx);
+        __syncwarp();
+        if (lane == 0) {
+          red[(rr * NCW + (wid - 1)) * 2] = sw;
+          red[(rr * NCW + (wid - 1)) * 2 + 1] = sx;
+          mbar_arrive(&ring->empty[st]);
+        }
+      }
+      asm volatile("bar.sync 1, %0;" :: "r"(32 * NCW) : "memory");
+      if (ct < 2 * rows) {
+        const int rr = ct >> 1, which = ct & 1;
+        double t = 0.0;
+        for (int q = 0; q < NCW; ++q) t += red[(rr * NCW + q) * 2 + which];
+        const int i = r0 + rr;
+        if (which == 0) { a.w[i] = t; Wp += t * t; }
+        else { a.ax[i] = t; const double y = a.b[i] - t; Yp += y * y; }
+      }
+      asm volatile("bar.sync 1, %0;" :: "r"(32 * NCW) : "memory");
+    }
+  }
+  u_ring += re - rb;                            // every thread: the ring's use counter
+  __syncthreads();
+}
+
 __device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp,
                               const double* in1 = nullptr, const double* in2 = nullptr,
                               double* out1 = nullptr, double* out2 = nullptr,
@@ -853,11 +959,15 @@ __device__ void p_zero_side(const PArgs& a, int side) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
   __shared__ __align__(16) unsigned int h[NBINS];
+  __shared__ __align__(8) TmaRing ring;
+  __shared__ __align__(8) unsigned long long tbar[(PT / TG) * TBUF];
   __shared__ double sh[PW];
   __shared__ unsigned int sh_u[4];
   __shared__ long long sh_l[40];
   __shared__ PSel ps;
-  extern __shared__ double dyn[];
+  extern __shared__ __align__(16) double dyn[];
+  TileRing tring{tbar + (threadIdx.x / TG) * TBUF, 0u};
+  if (!a.dense) tile_rings_init(tbar);
   Scal* st = a.st;
   TraceRec* tr = a.tr;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
@@ -882,6 +992,14 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
   unsigned long long t_last = 0;
   unsigned int bgen = 0;
   if (threadIdx.x == 0) bgen = ld_acquire_u32(&a.bar->gen);
+  long long u_ring = 0;
+  if (a.pn_tma) {
+    if (threadIdx.x == 0) {
+      for (int st = 0; st < a.pn_tma; ++st) { mbar_init(&ring.full[st], 1); mbar_init(&ring.empty[st], PW - 1); }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
 #define PH(i)                                                        \
   if (a.ptime && lead) {                                             \
     const unsigned long long t_ = gtimer();                          \
@@ -971,7 +1089,8 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       const ColKeyEpi ep{a.gamma, a.keys_n, h, k, seed, pending, a.greedy};
       const int g = threadIdx.x / TG;
       csr_tiles(blockIdx.x * (PT / TG) + g, G * (PT / TG), threadIdx.x % TG, 1 + g,
-                reinterpret_cast<TileSmem*>(dyn) + g, a.cp, a.ri, a.rv, a.tilesT, a.ntilesT,
+                reinterpret_cast<TileSmem*>(dyn) + g, tring, a.cp, a.ri, a.rv, a.tilesT,
+                a.tilepT, a.ntilesT,
                 a.z, a.xi, pending, nullptr, a.s, a.v, Vp, Emax, &ep, 0, a.vecT);
       __syncthreads();
       flush_hist<PT>(h, hn, NBINS);
@@ -996,9 +1115,13 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       p_sel_greedy(&ps, slot_max(bp, SL_MAXN, sh), a.eta);
     } else if (n <= LOCAL_SEL_MAX) {
       p_sel_level1(&ps, hn, n, kc, sh_u, sh_l);
+      PH(13);
       if (!p_sel_local_smem(&ps, a.keys_n, n, 0, hn, h, sh_u, sh_l, reinterpret_cast<Cand*>(dyn),
-                            reinterpret_cast<Cand*>(dyn) + LCAND_CAP))
+                            reinterpret_cast<Cand*>(dyn) + LCAND_CAP)) {
+        if (a.ptime && lead) a.ptime[16] += 1;
         p_sel_local(&ps, a.keys_n, n, 0, h, sh_u, sh_l);
+      }
+      PH(14);
     } else {
       p_sel_level1(&ps, hn, n, kc, sh_u, sh_l);
       p_sel_scan<2>(&ps, a.keys_n, n, 0, hn + NBINS, cn, a.ncand, h);
@@ -1052,11 +1175,17 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     {
       double Wp = 0.0, Yp = 0.0;
       if (a.dense) {
-        p_dense_passN(a, dyn, Wp, Yp);
+        const int kp3 = (a.n + 2 * 32 * (PW - 1) - 1) / (2 * 32 * (PW - 1));
+        if (a.pn_tma && kp3 == 1) p_dense_passN_tma<1>(a, dyn, &ring, a.pn_tma, u_ring, Wp, Yp);
+        else if (a.pn_tma && kp3 == 2) p_dense_passN_tma<2>(a, dyn, &ring, a.pn_tma, u_ring, Wp, Yp);
+        else if (a.pn_tma && kp3 == 3) p_dense_passN_tma<3>(a, dyn, &ring, a.pn_tma, u_ring, Wp, Yp);
+        else if (a.pn_tma && kp3 == 4) p_dense_passN_tma<4>(a, dyn, &ring, a.pn_tma, u_ring, Wp, Yp);
+        else p_dense_passN(a, dyn, Wp, Yp);
       } else {
         const int g = threadIdx.x / TG;
         csr_tiles(blockIdx.x * (PT / TG) + g, G * (PT / TG), threadIdx.x % TG, 1 + g,
-                  reinterpret_cast<TileSmem*>(dyn) + g, a.rp, a.ci, a.cv, a.tilesN, a.ntilesN,
+                  reinterpret_cast<TileSmem*>(dyn) + g, tring, a.rp, a.ci, a.cv, a.tilesN,
+                  a.tilepN, a.ntilesN,
                   a.zeta, a.x, 1, a.b, a.w, a.ax, Wp, Yp, nullptr, 0, a.vecN);
       }
       const double wb = pblock_sum(Wp, sh);
@@ -1130,8 +1259,11 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     } else if (m_loc <= LOCAL_SEL_MAX) {
       p_sel_level1(&ps, hm, m_loc, kr, sh_u, sh_l);
       if (!p_sel_local_smem(&ps, a.keys_m, m_loc, a.row0, hm, h, sh_u, sh_l,
-                            reinterpret_cast<Cand*>(dyn), reinterpret_cast<Cand*>(dyn) + LCAND_CAP))
+                            reinterpret_cast<Cand*>(dyn), reinterpret_cast<Cand*>(dyn) + LCAND_CAP)) {
+        if (a.ptime && lead) a.ptime[17] += 1;
         p_sel_local(&ps, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
+      }
+      PH(15);
     } else {
       p_sel_level1(&ps, hm, m_loc, kr, sh_u, sh_l);
       p_sel_scan<2>(&ps, a.keys_m, m_loc, a.row0, hm + NBINS, cm, a.ncand + 1, h);

@@ -59,6 +59,8 @@ struct rgdbek_ctx {
   double* rv = nullptr;
   int vecN = 8, vecT = 8;
   int* tilesN = nullptr;                // CSR row tiles (csr_tiles.cuh), [ntilesN + 1]
+  long long* tilepN = nullptr;          // first nonzero of each row tile, [ntilesN + 1]
+  long long* tilepT = nullptr;          // same for the CSC tiles
   int* tilesT = nullptr;                // CSC row tiles, [ntilesT + 1]
   int ntilesN = 0, ntilesT = 0;
   int tile_grid = 1;                    // resident 256-thread tile blocks
@@ -69,6 +71,7 @@ struct rgdbek_ctx {
   int engine = 0;                       // 0 = persistent cooperative kernel, 1 = graph engine
   int pG = 1;                           // persistent: CTAs
   size_t p_dyn = 0;                     // persistent: dynamic smem bytes
+  bool graph_built = false;             // graph engine captured (lazily for engine 0)
   PArgs pargs;                          // persistent: kernel arguments
   unsigned int* phist = nullptr;        // persistent: [2][3][NBINS]
   Cand* pcand = nullptr;                // persistent: [2][CAND_CAP]
@@ -143,7 +146,9 @@ rgdbek_status set_err(rgdbek_ctx* h, rgdbek_status code, const char* fmt, ...) {
 template <typename T>
 rgdbek_status dalloc(rgdbek_ctx* h, T** p, size_t count) {
   void* q = nullptr;
-  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  // 64 bytes of slack: the tile bulk copies widen their windows to 16-byte
+  // boundaries and may read up to 16 bytes past the last element
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T) + 64;
   cudaError_t e = cudaMalloc(&q, bytes);
   if (e != cudaSuccess)
     return set_err(h, RGDBEK_E_OOM, "cudaMalloc(%zu bytes) failed: %s", bytes,
@@ -271,7 +276,7 @@ __global__ void k_selmask_to_list(const unsigned char* mask, long long count, lo
 // Greedy row tiles: consecutive rows with <= TILE_NNZ nonzeros and <= TILE_ROWS rows
 // (a longer row is a tile by itself).
 rgdbek_status build_tiles(rgdbek_ctx* h, const long long* d_ptr, long long rows, int** out,
-                          int* nt) {
+                          long long** outp, int* nt) {
   std::vector<long long> rp(rows + 1);
   CK(h, cudaMemcpyAsync(rp.data(), d_ptr, (rows + 1) * sizeof(long long), cudaMemcpyDeviceToHost,
                         h->stream));
@@ -289,11 +294,18 @@ rgdbek_status build_tiles(rgdbek_ctx* h, const long long* d_ptr, long long rows,
     acc += len;
   }
   t.push_back((int)rows);
+  std::vector<long long> tp(t.size());
+  for (size_t i = 0; i < t.size(); ++i) tp[i] = rp[t[i]];
   int* d = nullptr;
+  long long* dp = nullptr;
   TRY(dalloc(h, &d, t.size()));
+  TRY(dalloc(h, &dp, tp.size()));
   CK(h, cudaMemcpyAsync(d, t.data(), t.size() * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(dp, tp.data(), tp.size() * sizeof(long long), cudaMemcpyHostToDevice,
+                        h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
   *out = d;
+  *outp = dp;
   *nt = (int)t.size() - 1;
   return RGDBEK_OK;
 }
@@ -344,7 +356,7 @@ void launch_passT(rgdbek_ctx* h) {
   } else {
     k_csr_tiles<1><<<std::min((h->ntilesT + NT / TG - 1) / (NT / TG), h->tile_grid), NT,
                      (NT / TG) * sizeof(TileSmem), h->stream>>>(
-        h->cp, h->ri, h->rv, h->tilesT, h->ntilesT, h->z, h->xi, nullptr, h->s, h->v, h->st,
+        h->cp, h->ri, h->rv, h->tilesT, h->tilepT, h->ntilesT, h->z, h->xi, nullptr, h->s, h->v, h->st,
         h->trace, h->bpart, h->vecT);
   }
 }
@@ -362,7 +374,7 @@ void launch_passN(rgdbek_ctx* h) {
   } else {
     k_csr_tiles<0><<<std::min((h->ntilesN + NT / TG - 1) / (NT / TG), h->tile_grid), NT,
                      (NT / TG) * sizeof(TileSmem), h->stream>>>(
-        h->rp, h->ci, h->cv, h->tilesN, h->ntilesN, h->zeta, h->x, h->b, h->w, h->ax, h->st,
+        h->rp, h->ci, h->cv, h->tilesN, h->tilepN, h->ntilesN, h->zeta, h->x, h->b, h->w, h->ax, h->st,
         h->trace, h->bpart, h->vecN);
   }
 }
@@ -538,6 +550,14 @@ plain:
   return RGDBEK_OK;
 }
 
+rgdbek_status ensure_graph(rgdbek_ctx* h) {
+  if (h->graph_built) return RGDBEK_OK;
+  TRY(build_graph(h));
+  if (h->nccl_fail) return set_err(h, RGDBEK_E_NCCL, "NCCL call failed while capturing the iteration graph");
+  h->graph_built = true;
+  return RGDBEK_OK;
+}
+
 // Persistent engine: geometry, buffers and the kernel argument block.
 rgdbek_status setup_persistent(rgdbek_ctx* h) {
   if (const char* e = getenv("RGDBEK_ENGINE")) {
@@ -549,7 +569,13 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
                      : (PT / TG) * sizeof(TileSmem);
   // local selections gather the level-1 bucket into (LCAND_CAP + FINAL_CAP) Cand of smem
   h->p_dyn = std::max(h->p_dyn, (size_t)(LCAND_CAP + FINAL_CAP) * sizeof(Cand));
-  int pn_smem = 0;
+  int pn_smem = 0, pn_tma = 0;
+  if (h->dense && getenv("RGDBEK_PN_TMA") && h->n <= 8 * 32 * (PW - 1)) {
+    const size_t rowb = (size_t)h->lda * sizeof(double);
+    const size_t redb = 32 * (PW - 1) * 2 * sizeof(double);
+    int st = (int)std::min<size_t>(TMA_STAGES_MAX, (200 * 1024 - redb) / rowb);
+    if (st >= 2) { pn_tma = st; h->p_dyn = std::max(h->p_dyn, st * rowb + redb); }
+  }
   if (h->dense) {
     // dense pass N stages zeta and x (2 x lda doubles) after its partials when they fit
     const size_t need = (size_t)PN_RB * PN_QMAX * 2 * sizeof(double) + 2 * (size_t)h->lda * sizeof(double);
@@ -605,15 +631,17 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
   a.part = ppart; a.bpart = h->bpart; a.hist = h->phist; a.cand = h->pcand; a.acc = h->pacc;
   a.ncand = h->pncand; a.st = h->st; a.tr = h->trace; a.bar = h->pbar;
   a.tilesN = h->tilesN; a.tilesT = h->tilesT; a.ntilesN = h->ntilesN; a.ntilesT = h->ntilesT;
+  a.tilepN = h->tilepN; a.tilepT = h->tilepT;
   a.greedy = 0;
   a.eta = h->eta;
   a.pn_smem = pn_smem;
+  a.pn_tma = pn_tma;
   // one-sweep register-column pass T measured slower (223 vs 129 us on C2c): opt-in
   a.pt_rows = getenv("RGDBEK_PT_ROWS") ? 1 : 0;
   if (const char* e = getenv("RGDBEK_PHASE_TIMING")) {
     if (atoi(e)) {
-      TRY(dalloc(h, &h->ptime, 16));
-      CK(h, cudaMemsetAsync(h->ptime, 0, 16 * sizeof(unsigned long long), h->stream));
+      TRY(dalloc(h, &h->ptime, 24));
+      CK(h, cudaMemsetAsync(h->ptime, 0, 24 * sizeof(unsigned long long), h->stream));
       a.ptime = h->ptime;
     }
   }
@@ -673,8 +701,9 @@ rgdbek_status finish_create(rgdbek_ctx* h) {
   CK(h, cudaEventCreate(&h->ev0));
   CK(h, cudaEventCreate(&h->ev1));
   TRY(setup_persistent(h));
-  TRY(build_graph(h));
-  if (h->nccl_fail) return set_err(h, RGDBEK_E_NCCL, "NCCL call failed while capturing the iteration graph");
+  // the graph engine is captured at create only when it is the engine in use
+  // (multi-GPU or RGDBEK_ENGINE=graph); the persistent engine never needs it
+  if (h->engine != 0) TRY(ensure_graph(h));
   CK(h, cudaStreamSynchronize(h->stream));
   return RGDBEK_OK;
 }
@@ -751,11 +780,12 @@ rgdbek_status common_begin(rgdbek_ctx* h, long long m, long long n, const rgdbek
                    cudaGetErrorString(e));
   if (h->device < 0 || h->device >= ndev) return set_err(h, RGDBEK_E_ARG, "device %d out of range", h->device);
   CK(h, cudaSetDevice(h->device));
-  cudaDeviceProp prop;
-  CK(h, cudaGetDeviceProperties(&prop, h->device));
-  if (prop.major < 10)
-    return set_err(h, RGDBEK_E_CUDA, "device %s is sm_%d%d; this library is built for sm_100a",
-                   prop.name, prop.major, prop.minor);
+  int cc_major = 0, cc_minor = 0;
+  CK(h, cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, h->device));
+  CK(h, cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, h->device));
+  if (cc_major < 10)
+    return set_err(h, RGDBEK_E_CUDA, "device %d is sm_%d%d; this library is built for sm_100a",
+                   h->device, cc_major, cc_minor);
   if (o->stream) {
     h->stream = (cudaStream_t)o->stream;
   } else {
@@ -829,6 +859,7 @@ rgdbek_status ensure_usable(rgdbek_ctx* h) {
 
 rgdbek_status run_loop(rgdbek_ctx* h, rgdbek_result* res) {
   CK(h, cudaEventRecord(h->ev0, h->stream));
+  if (h->engine != 0) TRY(ensure_graph(h));
   if (h->engine == 0) {
     TRY(launch_persistent(h));
   } else if (h->use_cond) {
@@ -1036,10 +1067,10 @@ rgdbek_status rgdbek_create_csr(rgdbek_handle* out, int64_t m, int64_t n, int64_
     const int v = atoi(e);
     if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) h->vecN = h->vecT = v;
   }
-  if ((s = build_tiles(h, h->rp, h->m_loc, &h->tilesN, &h->ntilesN)) != RGDBEK_OK) return create_fail(h, s);
+  if ((s = build_tiles(h, h->rp, h->m_loc, &h->tilesN, &h->tilepN, &h->ntilesN)) != RGDBEK_OK) return create_fail(h, s);
   if (h->cp == h->rp) {
-    h->tilesT = h->tilesN; h->ntilesT = h->ntilesN;
-  } else if ((s = build_tiles(h, h->cp, h->n, &h->tilesT, &h->ntilesT)) != RGDBEK_OK) {
+    h->tilesT = h->tilesN; h->tilepT = h->tilepN; h->ntilesT = h->ntilesN;
+  } else if ((s = build_tiles(h, h->cp, h->n, &h->tilesT, &h->tilepT, &h->ntilesT)) != RGDBEK_OK) {
     return create_fail(h, s);
   }
   {
@@ -1206,6 +1237,8 @@ rgdbek_status rgdbek_launch_kernel(rgdbek_handle h, int32_t kernel, int32_t reps
 
 rgdbek_status rgdbek_launches_per_iteration(rgdbek_handle h, int64_t* out) {
   if (!h || !out) return RGDBEK_E_ARG;
+  if (h->engine == 0) { *out = 0; return RGDBEK_OK; }
+  TRY(ensure_graph(h));
   *out = h->launches_per_iter;
   return RGDBEK_OK;
 }
@@ -1217,9 +1250,9 @@ rgdbek_status rgdbek_phase_times(rgdbek_handle h, double* out_ns, int32_t max_ph
   TRY(ensure_usable(h));
   if (!out_ns || !n_out || max_phases < 0) return set_err(h, RGDBEK_E_ARG, "bad arguments");
   if (!h->ptime || h->engine != 0) { *n_out = 0; return RGDBEK_OK; }
-  unsigned long long t[16];
+  unsigned long long t[24];
   CK(h, cudaMemcpy(t, h->ptime, sizeof t, cudaMemcpyDeviceToHost));
-  const int cnt = std::min(16, (int)max_phases);
+  const int cnt = std::min(24, (int)max_phases);
   for (int i = 0; i < cnt; ++i) out_ns[i] = (double)t[i];
   *n_out = cnt;
   return RGDBEK_OK;

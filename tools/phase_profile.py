@@ -14,7 +14,8 @@ sys.path.insert(0, ROOT)
 
 PHASES = {1: "passT", 2: "s_v_colkeys_L1", 3: "colsel_L2", 4: "colsel_L3", 5: "mask_x_update",
           6: "passN", 7: "stop_z_rowkeys_L1", 8: "rowsel_L2", 9: "rowsel_L3", 10: "row_mask",
-          0: "bookkeeping", 11: "dense_P2_columns", 12: "dense_P2_flush_sum"}
+          0: "bookkeeping", 11: "dense_P2_columns", 12: "dense_P2_flush_sum",
+          13: "colsel_local_L1", 14: "colsel_local_L2L3", 15: "rowsel_local"}
 
 
 def main():
@@ -41,6 +42,8 @@ def main():
             iters = steps + 5 + 2   # phase timers accumulate over every launch on the handle
             out["us_per_iter"] = {PHASES[i]: round(t[i] / 1e3 / iters, 2) for i in PHASES}
             out["us_per_iter_total"] = round(sum(t[i] for i in PHASES) / 1e3 / iters, 2)
+            if len(t) > 17:
+                out["local_sel_overflows"] = {"col": int(t[16]), "row": int(t[17])}
         s.close()
     print(json.dumps(out))
 
