@@ -62,7 +62,8 @@ def load(path=None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    # RGDBEK_LIB: an explicitly built variant of the library (tools/ab_variants.py)
+    path = path or os.environ.get("RGDBEK_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(f"{path} is missing: build it with __graft_entry__.build() "
                            "(there is no CPU fallback)")

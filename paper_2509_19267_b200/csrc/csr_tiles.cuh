@@ -21,10 +21,31 @@
 
 namespace rg {
 
+// Geometry (compile-time; -D overrides exist for A/B builds, tools/ab_variants.py).
+#ifndef RG_TILE_NNZ
+#define RG_TILE_NNZ 512
+#endif
+#ifndef RG_TILE_ROWS
+#define RG_TILE_ROWS 96
+#endif
+#ifndef RG_TBUF
+#define RG_TBUF 3
+#endif
+#ifndef RG_PEND
+#define RG_PEND 256
+#endif
+#ifndef RG_RU
+#define RG_RU 6
+#endif
+#ifndef RG_TILE_BLOCKED
+#define RG_TILE_BLOCKED 0
+#endif
 constexpr int TG = 128;              // threads per worker group
-constexpr int TILE_NNZ = 512;        // nonzeros per tile
-constexpr int TILE_ROWS = 128;       // rows per tile
-constexpr int TBUF = 3;              // tiles in flight per group
+constexpr int TILE_NNZ = RG_TILE_NNZ;    // nonzeros per tile
+constexpr int TILE_ROWS = RG_TILE_ROWS;  // rows per tile
+constexpr int TBUF = RG_TBUF;        // staged tiles per group (one in use, the rest in flight)
+constexpr int TRING = 2 * TBUF;      // mbarriers per group: full[TBUF], empty[TBUF]
+constexpr int PEND = RG_PEND;        // pass-T columns batched for the key epilogue
 
 // One staged tile.  Windows are widened to 16-byte boundaries (bulk-copy
 // alignment): val from p0 & ~1, idx from p0 & ~3, rp from r0 & ~1.
@@ -38,8 +59,8 @@ static_assert(sizeof(TileBuf) % 16 == 0, "TileBuf must keep 16-byte alignment");
 // Pass-T column results waiting for the key epilogue (batched so a tile of a
 // few long columns does not run the ALU-heavy key chain on a few threads).
 struct TilePend {
-  double s1[TG], s2[TG];
-  int row[TG];
+  double s1[PEND], s2[PEND];
+  int row[PEND];
 };
 
 struct __align__(16) TileSmem {
@@ -54,24 +75,29 @@ __device__ __forceinline__ void group_bar(int id) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(TG) : "memory");
 }
 
-// Per-group ring state: TBUF "full" mbarriers (in static shared memory, so
-// other phases may reuse the TileSmem area as scratch) and the number of
-// tiles this group has consumed so far (identical in all its threads).
+// Per-group ring state: TRING mbarriers in static shared memory (so other
+// phases may reuse the TileSmem area as scratch) — full[b] completes when
+// buffer b's bulk copies have landed, empty[b] when the group's TG/32 warps
+// have released it — and the number of tiles this group has consumed so far
+// (identical in all its threads).
 struct TileRing {
-  unsigned long long* full;   // [TBUF]
+  unsigned long long* full;   // [TRING]: full[0..TBUF), then empty[0..TBUF)
   unsigned int used;
 };
 
 // Initialise a group's barriers (one thread), before the first csr_tiles call;
 // the caller follows with fence.mbarrier_init + a CTA barrier.
-__device__ __forceinline__ void tile_ring_init(unsigned long long* full) {
-  for (int i = 0; i < TBUF; ++i) mbar_init(&full[i], 1);
+__device__ __forceinline__ void tile_ring_init(unsigned long long* bars) {
+  for (int i = 0; i < TBUF; ++i) {
+    mbar_init(&bars[i], 1);
+    mbar_init(&bars[TBUF + i], TG / 32);
+  }
 }
 
 // CTA prologue of a kernel running csr_tiles: every group's barriers, made
 // visible to the async proxy and to the whole CTA.
 __device__ __forceinline__ void tile_rings_init(unsigned long long* bars) {
-  if (threadIdx.x % TG == 0) tile_ring_init(bars + (threadIdx.x / TG) * TBUF);
+  if (threadIdx.x % TG == 0) tile_ring_init(bars + (threadIdx.x / TG) * TRING);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
 }
@@ -149,12 +175,12 @@ __device__ __forceinline__ void tile_row_out(int row, double s1, double s2, bool
   if (acc1) Wp += s1 * s1;
 }
 
-// Key epilogue of the pending pass-T columns (thread lt takes entry lt).
+// Key epilogue of the pending pass-T columns (thread lt takes entries lt, lt + TG).
 __device__ __forceinline__ void tile_flush(const ColKeyEpi* ep, TilePend* pd, int npend, int lt,
                                            double& Vp, double& Emax) {
-  if (lt < npend) {
-    const int j = pd->row[lt];
-    colkey_epilogue(ep, j, pd->s1[lt], pd->s2[lt], Vp, Emax, ep->gamma[j]);
+  for (int e = lt; e < npend; e += TG) {
+    const int j = pd->row[e];
+    colkey_epilogue(ep, j, pd->s1[e], pd->s2[e], Vp, Emax, ep->gamma[j]);
   }
 }
 
@@ -166,15 +192,28 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
                           const double* __restrict__ b, double* o1, double* o2,
                           double& Wp, double& Yp,
                           const ColKeyEpi* ep = nullptr, int acc1 = 0, int vec = 1) {
+  // default: tiles gid, gid + ngroups, ...: at any moment the groups of the
+  // whole GPU stream one contiguous window of the matrix (measured faster on C3
+  // than a contiguous run of tiles per group, RG_TILE_BLOCKED=1)
+#if RG_TILE_BLOCKED
+  const int tb = (int)((long long)ntiles * gid / ngroups), tstep = 1;
+  const int cnt = (int)((long long)ntiles * (gid + 1) / ngroups) - tb;
+#else
+  const int tb = gid, tstep = ngroups;
   const int cnt = gid < ntiles ? (ntiles - gid + ngroups - 1) / ngroups : 0;
+#endif
   // the staging buffers may have been scratch of another phase (generic-proxy
   // writes): order those before the async-proxy (TMA) writes below
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   group_bar(bar_id);
+  unsigned long long* full = ring.full;
+  unsigned long long* empty = ring.full + TBUF;
   if (lt == 0) {
     for (int i = 0; i < cnt && i < TBUF; ++i) {
       const unsigned u = ring.used + i;
-      tile_issue(sm, u % TBUF, &ring.full[u % TBUF], tile_desc(gid + i * ngroups, tiles, tilep),
+      // buffer reuse across calls: the previous call's last uses were released
+      if (u >= TBUF) mbar_wait(&empty[u % TBUF], (u / TBUF - 1) & 1u);
+      tile_issue(sm, u % TBUF, &full[u % TBUF], tile_desc(tb + i * tstep, tiles, tilep),
                  ptr, idx, val);
     }
   }
@@ -182,16 +221,17 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
   const bool has_b = b != nullptr;
   int npend = 0;                                   // pass T: columns awaiting their keys
   for (int i = 0; i < cnt; ++i) {
-    const int t = gid + i * ngroups;
+    const int t = tb + i * tstep;
     const unsigned u = ring.used + i, bi = u % TBUF;
     // the producer fetches the descriptor of the tile it refills this buffer with
     TileDesc nd{0, 0, 0, 0};
     const bool refill = lt == 0 && i + TBUF < cnt;
-    if (refill) nd = tile_desc(t + TBUF * ngroups, tiles, tilep);
-    mbar_wait(&ring.full[bi], (u / TBUF) & 1u);
+    if (refill) nd = tile_desc(t + TBUF * tstep, tiles, tilep);
+    mbar_wait(&full[bi], (u / TBUF) & 1u);
     const int r0 = (int)sm->desc[bi][0], nr = (int)(sm->desc[bi][1] - sm->desc[bi][0]);
     const long long p0 = sm->desc[bi][2], p1 = sm->desc[bi][3];
-    if (ep && npend + nr > TG) {                   // make room in the pending list
+    if (ep && npend + nr > PEND) {                 // make room in the pending list
+      group_bar(bar_id);                           // every warp's entries are written
       tile_flush(ep, &sm->pend, npend, lt, Wp, Yp);
       npend = 0;
       group_bar(bar_id);
@@ -220,6 +260,7 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
           tile_row_out(r0, s1, s2, has_b, bv, o1, o2, Wp, Yp, acc1);
         }
       }
+      group_bar(bar_id);                           // red[] is free for the next long row
     } else {
       // lanes per row for this tile: the mean-length choice `vec`, raised so the
       // tile's rows cover the whole group (a tile of few long rows still keeps
@@ -239,24 +280,27 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
         if (valid) {
           int q = (int)(R[r] - p0) + sl;
           const int q1 = (int)(R[r + 1] - p0);
-          for (; q + 3 * v < q1; q += 4 * v) {       // four entries: gathers in flight together
-            double a[4], g1[4], g2[4];
+          // RU entries per lane per round, predicated: one gather round trip
+          // covers a whole row of up to RU * v entries
+          constexpr int RU = RG_RU;
+          for (; q < q1; q += RU * v) {
+            int c[RU];
+            double g1[RU], g2[RU];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) a[e] = V[q + e * v];
+            for (int e = 0; e < RU; ++e) c[e] = q + e * v < q1 ? I[q + e * v] : -1;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int c = I[q + e * v];
-              g1[e] = ld_weak(in1 + c);
-              g2[e] = use2 ? ld_weak(in2 + c) : 0.0;
+            for (int e = 0; e < RU; ++e) {
+              g1[e] = c[e] >= 0 ? in1[c[e]] : 0.0;
+              g2[e] = (use2 && c[e] >= 0) ? in2[c[e]] : 0.0;
             }
 #pragma unroll
-            for (int e = 0; e < 4; ++e) { s1 = fma(a[e], g1[e], s1); s2 = fma(a[e], g2[e], s2); }
-          }
-          for (; q < q1; q += v) {
-            const double a = V[q];
-            const int c = I[q];
-            s1 = fma(a, ld_weak(in1 + c), s1);
-            if (use2) s2 = fma(a, ld_weak(in2 + c), s2);
+            for (int e = 0; e < RU; ++e) {
+              if (c[e] >= 0) {
+                const double a = V[q + e * v];
+                s1 = fma(a, g1[e], s1);
+                s2 = fma(a, g2[e], s2);
+              }
+            }
           }
         }
         for (int o = v >> 1; o > 0; o >>= 1) {
@@ -275,10 +319,19 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
       }
     }
     npend += nr;
-    group_bar(bar_id);                              // buffer bi free again; pend entries visible
-    if (refill) tile_issue(sm, bi, &ring.full[bi], nd, ptr, idx, val);
+    // release buffer bi (each warp once its lanes are done with it); the
+    // warps then run ahead to the next staged tile without a group barrier
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[bi]);
+    if (refill) {
+      mbar_wait(&empty[bi], (u / TBUF) & 1u);
+      tile_issue(sm, bi, &full[bi], nd, ptr, idx, val);
+    }
   }
-  if (ep) tile_flush(ep, &sm->pend, npend, lt, Wp, Yp);
+  if (ep) {
+    group_bar(bar_id);
+    tile_flush(ep, &sm->pend, npend, lt, Wp, Yp);
+  }
   ring.used += cnt;
 }
 

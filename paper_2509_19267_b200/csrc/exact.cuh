@@ -67,9 +67,10 @@ __device__ void ex_dense_colreduce(const PArgs& a, int use2, double* o1, double*
 }
 
 // o1 = A^T in1 (and o2 = A^T in2 when use2) over all columns; ends after a grid barrier.
+template <bool DENSE>
 __device__ void ex_passT(const PArgs& a, TileRing& ring, const double* in1, const double* in2, int use2,
                          double* o1, double* o2, double* dyn, unsigned int& bgen) {
-  if (a.dense) {
+  if constexpr (DENSE) {
     p_dense_passT(a, use2, dyn, in1, in2);
     grid_sync(a.bar, bgen);
     ex_dense_colreduce(a, use2, o1, o2, dyn);
@@ -86,9 +87,10 @@ __device__ void ex_passT(const PArgs& a, TileRing& ring, const double* in1, cons
 
 // o1 = A in1, o2 = A in2 over this rank's rows.  W += o1^2; Y += (b - o2)^2 if b else o2^2.
 // No barrier at the end (the caller publishes W / Y partials first).
+template <bool DENSE>
 __device__ void ex_passN(const PArgs& a, TileRing& ring, const double* in1, const double* in2, double* o1,
                          double* o2, const double* bvec, double& Wp, double& Yp, double* dyn) {
-  if (a.dense) {
+  if constexpr (DENSE) {
     p_dense_passN(a, dyn, Wp, Yp, in1, in2, o1, o2, bvec, bvec != nullptr);
   } else {
     const int g = threadIdx.x / TG;
@@ -112,16 +114,17 @@ __device__ __forceinline__ void ex_allsum2(const PArgs& a, double p1, double p2,
   s2 = slot_sum(a.bpart, slot2, sh);
 }
 
+template <bool DENSE>
 __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
   __shared__ __align__(16) unsigned int h[NBINS];
-  __shared__ __align__(8) unsigned long long tbar[(PT / TG) * TBUF];
+  __shared__ __align__(8) unsigned long long tbar[(PT / TG) * TRING];
   __shared__ double sh[PW];
   __shared__ unsigned int sh_u[4];
   __shared__ long long sh_l[40];
   __shared__ PSel ps;
   extern __shared__ __align__(16) double dyn[];
-  TileRing ring{tbar + (threadIdx.x / TG) * TBUF, 0u};
-  if (!a.dense) tile_rings_init(tbar);
+  TileRing ring{tbar + (threadIdx.x / TG) * TRING, 0u};
+  if (!DENSE) tile_rings_init(tbar);
   Scal* st = a.st;
   TraceRec* tr = a.tr;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
   {
     double Wd = 0.0, Yp = 0.0;
     ++npass;
-    ex_passN(a, ring, a.x, a.x, e.u, a.ax, a.b, Wd, Yp, dyn);
+    ex_passN<DENSE>(a, ring, a.x, a.x, e.u, a.ax, a.b, Wd, Yp, dyn);
     double Wsum;
     ex_allsum2(a, Wd, Yp, SL_W, SL_Y, sh, bgen, Wsum, Yk);
   }
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
     __syncthreads();
     ++npass;
-    ex_passT(a, ring, a.z, a.z, 0, a.s, a.v, dyn, bgen);                 // s = A^T z_k
+    ex_passT<DENSE>(a, ring, a.z, a.z, 0, a.s, a.v, dyn, bgen);                 // s = A^T z_k
     p_zero_side(a, 1);
     double Emax = 0.0;
     for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) {
@@ -232,7 +235,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     for (int it = 0; it < e.inner_max && kp > 0 && gam > 0.0; ++it) {
       double Wp = 0.0, Yd = 0.0;
       ++npass;
-      ex_passN(a, ring, a.zeta, a.zeta, a.w, e.u, nullptr, Wp, Yd, dyn);           // q = A p
+      ex_passN<DENSE>(a, ring, a.zeta, a.zeta, a.w, e.u, nullptr, Wp, Yd, dyn);           // q = A p
       double Wq, d2;
       ex_allsum2(a, Wp, 0.0, SL_W, SL_Y, sh, bgen, Wq, d2);
       if (it == 0) W0 = Wq;
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
       if (it + 1 == e.inner_max) break;
       grid_sync(a.bar, bgen);
       ++npass;
-      ex_passT(a, ring, a.z, a.z, 0, a.s, a.v, dyn, bgen);                         // s' = A^T z
+      ex_passT<DENSE>(a, ring, a.z, a.z, 0, a.s, a.v, dyn, bgen);                         // s' = A^T z
       double gp = 0.0;
       for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT)
         if (p_selected(&ps, a.keys_n[j], j)) gp += a.s[j] * a.s[j];
@@ -328,7 +331,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     double V0 = 0.0;
     if (kpp > 0 && X > 0.0) {
       ++npass;
-      ex_passT(a, ring, a.xi, a.xi, 0, a.v, a.s, dyn, bgen);                      // t = A^T r_J
+      ex_passT<DENSE>(a, ring, a.xi, a.xi, 0, a.v, a.s, dyn, bgen);                      // t = A^T r_J
       double gp = 0.0;
       for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) {
         const double t = a.v[j];
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
       for (int it = 0; it < e.inner_max && gam > 0.0; ++it) {
         double Wd = 0.0, Yd = 0.0;
         ++npass;
-        ex_passN(a, ring, e.px, e.px, e.u, a.w, nullptr, Wd, Yd, dyn);            // u = A p
+        ex_passN<DENSE>(a, ring, e.px, e.px, e.u, a.w, nullptr, Wd, Yd, dyn);            // u = A p
         grid_sync(a.bar, bgen);   // sparse tiles spread rows over all CTAs
         double qp = 0.0;
         for (int i = blockIdx.x * PT + threadIdx.x; i < m_loc; i += G * PT)
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
         if (it + 1 == e.inner_max) break;
         grid_sync(a.bar, bgen);
         ++npass;
-        ex_passT(a, ring, a.xi, a.xi, 0, a.v, a.s, dyn, bgen);                    // t = A^T r_J
+        ex_passT<DENSE>(a, ring, a.xi, a.xi, 0, a.v, a.s, dyn, bgen);                    // t = A^T r_J
         double gq = 0.0;
         for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) gq += a.v[j] * a.v[j];
         double gnew, d7;
@@ -380,7 +383,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     {
       double Wd = 0.0, Yp = 0.0, Rp = 0.0;
       ++npass;
-      ex_passN(a, ring, a.x, a.x, e.u, a.ax, a.b, Wd, Yp, dyn);
+      ex_passN<DENSE>(a, ring, a.x, a.x, e.u, a.ax, a.b, Wd, Yp, dyn);
       if (has_ref)
         for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) {
           const double d = a.x[j] - a.xstar[j];

@@ -262,9 +262,9 @@ __global__ void __launch_bounds__(NT) k_csr_tiles(const long long* __restrict__ 
   const int g = threadIdx.x / TG;
   TileSmem* sm = reinterpret_cast<TileSmem*>(tsm_raw) + g;
   __shared__ double sh[NT / 32];
-  __shared__ __align__(8) unsigned long long tbar[GPB * TBUF];
+  __shared__ __align__(8) unsigned long long tbar[GPB * TRING];
   tile_rings_init(tbar);
-  TileRing ring{tbar + g * TBUF, 0u};
+  TileRing ring{tbar + g * TRING, 0u};
   const int use2 = (MODE == 1) ? st->pending : 1;
   double Wp = 0.0, Yp = 0.0;
   csr_tiles(blockIdx.x * GPB + g, gridDim.x * GPB, threadIdx.x % TG, 1 + g, sm, ring, ptr, idx,

@@ -59,7 +59,6 @@ struct PArgs {
   double eta;
   int pn_smem;                      // dense pass N: zeta / x staged in shared memory
   int pt_rows;                      // dense pass T: one-sweep register-column form
-  int pn_tma;                       // dense pass N: TMA ring stages (0 = off)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -681,100 +680,6 @@ __device__ void p_dense_passT_rows(const PArgs& a, int pending, double* zs, cons
 // (1 row) x (column chunk of CH), partials in smem, summed in chunk order.
 // Returns this thread's contributions to W and ||b - Ax||^2.
 // ---------------------------------------------------------------------------
-// ---------------------------------------------------------------------------
-// Dense pass N with a TMA bulk-copy pipeline (RGDBEK_PN_TMA=1): warp 0 lane 0
-// streams the CTA's rows of A into a ring of S shared-memory stages with
-// cp.async.bulk (completion on an mbarrier, expect_tx), so the HBM stream never
-// waits for the math; warps 1..31 own fixed column pairs with zeta / x in
-// registers, read each row from shared memory, reduce per warp with shuffles,
-// release the stage, and every 32 rows add the 31 warp partials of each row in
-// warp order (deterministic).  Ring state persists across calls (u_prod, u_cons).
-// ---------------------------------------------------------------------------
-constexpr int TMA_STAGES_MAX = 8;
-struct TmaRing {
-  unsigned long long full[TMA_STAGES_MAX];
-  unsigned long long empty[TMA_STAGES_MAX];
-};
-
-template <int KP>
-__device__ void p_dense_passN_tma(const PArgs& a, double* dyn, TmaRing* ring, int S,
-                                  long long& u_ring, double& Wp, double& Yp) {
-  const int G = gridDim.x, bb = blockIdx.x;
-  const int rb = (int)((long long)a.m_loc * bb / G), re = (int)((long long)a.m_loc * (bb + 1) / G);
-  const int n = a.n;
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const unsigned rowbytes = (unsigned)(a.lda * sizeof(double));
-  double* stage0 = dyn;                                           // S x lda doubles
-  double* red = dyn + (long long)S * a.lda;                       // [32 rows][31 warps][2]
-  constexpr int NCW = PW - 1;                                     // consumer warps
-  if (wid == 0) {
-    // ---- producer ----
-    if (lane == 0) {
-      for (int i = rb; i < re; ++i) {
-        const long long u = u_ring + (i - rb);
-        const int st = (int)(u % S);
-        if (u >= S) mbar_wait(&ring->empty[st], (unsigned)(((u / S) - 1) & 1));
-        mbar_expect_tx(&ring->full[st], rowbytes);
-        bulk_g2s(stage0 + (long long)st * a.lda, a.A + (long long)i * a.lda, rowbytes, &ring->full[st]);
-      }
-    }
-    __syncwarp();
-  } else {
-    // ---- consumers ----
-    const int ct = threadIdx.x - 32;                              // 0 .. 991
-    double2 zr[KP], xr[KP];
-    bool ok[KP];
-#pragma unroll
-    for (int k = 0; k < KP; ++k) {
-      const int c = 2 * ct + 2 * 32 * NCW * k;
-      ok[k] = c + 1 < n;
-      zr[k] = ok[k] ? *reinterpret_cast<const double2*>(a.zeta + c) : make_double2(0.0, 0.0);
-      xr[k] = ok[k] ? *reinterpret_cast<const double2*>(a.x + c) : make_double2(0.0, 0.0);
-    }
-    const bool odd = (n & 1) && ct == 0;
-    const double zl = odd ? a.zeta[n - 1] : 0.0, xl = odd ? a.x[n - 1] : 0.0;
-    for (int r0 = rb; r0 < re; r0 += 32) {
-      const int rows = min(32, re - r0);
-      for (int rr = 0; rr < rows; ++rr) {
-        const long long u = u_ring + (r0 + rr - rb);
-        const int st = (int)(u % S);
-        mbar_wait(&ring->full[st], (unsigned)((u / S) & 1));
-        const double* row = stage0 + (long long)st * a.lda;
-        double sw = 0.0, sx = 0.0;
-#pragma unroll
-        for (int k = 0; k < KP; ++k) {
-          if (ok[k]) {
-            const double2 v = *reinterpret_cast<const double2*>(row + 2 * ct + 2 * 32 * NCW * k);
-            sw = fma(v.x, zr[k].x, sw); sw = fma(v.y, zr[k].y, sw);
-            sx = fma(v.x, xr[k].x, sx); sx = fma(v.y, xr[k].y, sx);
-          }
-        }
-        if (odd) { const double v = row[n - 1]; sw = fma(v, zl, sw); sx = fma(v, xl, sx); }
-        sw = warp_sum(sw);
-        sx = warp_sum(sx);
-        __syncwarp();
-        if (lane == 0) {
-          red[(rr * NCW + (wid - 1)) * 2] = sw;
-          red[(rr * NCW + (wid - 1)) * 2 + 1] = sx;
-          mbar_arrive(&ring->empty[st]);
-        }
-      }
-      asm volatile("bar.sync 1, %0;" :: "r"(32 * NCW) : "memory");
-      if (ct < 2 * rows) {
-        const int rr = ct >> 1, which = ct & 1;
-        double t = 0.0;
-        for (int q = 0; q < NCW; ++q) t += red[(rr * NCW + q) * 2 + which];
-        const int i = r0 + rr;
-        if (which == 0) { a.w[i] = t; Wp += t * t; }
-        else { a.ax[i] = t; const double y = a.b[i] - t; Yp += y * y; }
-      }
-      asm volatile("bar.sync 1, %0;" :: "r"(32 * NCW) : "memory");
-    }
-  }
-  u_ring += re - rb;                            // every thread: the ring's use counter
-  __syncthreads();
-}
-
 __device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp,
                               const double* in1 = nullptr, const double* in2 = nullptr,
                               double* out1 = nullptr, double* out2 = nullptr,
@@ -957,17 +862,20 @@ __device__ void p_zero_side(const PArgs& a, int side) {
 // ---------------------------------------------------------------------------
 // The persistent kernel.
 // ---------------------------------------------------------------------------
+// DENSE selects the pass kernels at compile time: each instantiation carries
+// only its own pass code, so the register allocation (64 per thread at 1024
+// threads) is not shared between the dense and the sparse paths.
+template <bool DENSE>
 __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
   __shared__ __align__(16) unsigned int h[NBINS];
-  __shared__ __align__(8) TmaRing ring;
-  __shared__ __align__(8) unsigned long long tbar[(PT / TG) * TBUF];
+  __shared__ __align__(8) unsigned long long tbar[(PT / TG) * TRING];
   __shared__ double sh[PW];
   __shared__ unsigned int sh_u[4];
   __shared__ long long sh_l[40];
   __shared__ PSel ps;
   extern __shared__ __align__(16) double dyn[];
-  TileRing tring{tbar + (threadIdx.x / TG) * TBUF, 0u};
-  if (!a.dense) tile_rings_init(tbar);
+  TileRing tring{tbar + (threadIdx.x / TG) * TRING, 0u};
+  if (!DENSE) tile_rings_init(tbar);
   Scal* st = a.st;
   TraceRec* tr = a.tr;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
@@ -992,14 +900,6 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
   unsigned long long t_last = 0;
   unsigned int bgen = 0;
   if (threadIdx.x == 0) bgen = ld_acquire_u32(&a.bar->gen);
-  long long u_ring = 0;
-  if (a.pn_tma) {
-    if (threadIdx.x == 0) {
-      for (int st = 0; st < a.pn_tma; ++st) { mbar_init(&ring.full[st], 1); mbar_init(&ring.empty[st], PW - 1); }
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-  }
 #define PH(i)                                                        \
   if (a.ptime && lead) {                                             \
     const unsigned long long t_ = gtimer();                          \
@@ -1013,7 +913,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     // Sparse: the column scores, keys, level-1 histogram and V partial are fused
     // into the tile epilogue, so the separate P2 phase (and its barrier) vanishes.
     double Vp = 0.0, Emax = 0.0;
-    if (a.dense) {
+    if constexpr (DENSE) {
       p_dense_passT(a, pending, dyn);
       grid_sync(a.bar, bgen);
       PH(1);
@@ -1174,13 +1074,8 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     }
     {
       double Wp = 0.0, Yp = 0.0;
-      if (a.dense) {
-        const int kp3 = (a.n + 2 * 32 * (PW - 1) - 1) / (2 * 32 * (PW - 1));
-        if (a.pn_tma && kp3 == 1) p_dense_passN_tma<1>(a, dyn, &ring, a.pn_tma, u_ring, Wp, Yp);
-        else if (a.pn_tma && kp3 == 2) p_dense_passN_tma<2>(a, dyn, &ring, a.pn_tma, u_ring, Wp, Yp);
-        else if (a.pn_tma && kp3 == 3) p_dense_passN_tma<3>(a, dyn, &ring, a.pn_tma, u_ring, Wp, Yp);
-        else if (a.pn_tma && kp3 == 4) p_dense_passN_tma<4>(a, dyn, &ring, a.pn_tma, u_ring, Wp, Yp);
-        else p_dense_passN(a, dyn, Wp, Yp);
+      if constexpr (DENSE) {
+        p_dense_passN(a, dyn, Wp, Yp);
       } else {
         const int g = threadIdx.x / TG;
         csr_tiles(blockIdx.x * (PT / TG) + g, G * (PT / TG), threadIdx.x % TG, 1 + g,

@@ -569,13 +569,7 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
                      : (PT / TG) * sizeof(TileSmem);
   // local selections gather the level-1 bucket into (LCAND_CAP + FINAL_CAP) Cand of smem
   h->p_dyn = std::max(h->p_dyn, (size_t)(LCAND_CAP + FINAL_CAP) * sizeof(Cand));
-  int pn_smem = 0, pn_tma = 0;
-  if (h->dense && getenv("RGDBEK_PN_TMA") && h->n <= 8 * 32 * (PW - 1)) {
-    const size_t rowb = (size_t)h->lda * sizeof(double);
-    const size_t redb = 32 * (PW - 1) * 2 * sizeof(double);
-    int st = (int)std::min<size_t>(TMA_STAGES_MAX, (200 * 1024 - redb) / rowb);
-    if (st >= 2) { pn_tma = st; h->p_dyn = std::max(h->p_dyn, st * rowb + redb); }
-  }
+  int pn_smem = 0;
   if (h->dense) {
     // dense pass N stages zeta and x (2 x lda doubles) after its partials when they fit
     const size_t need = (size_t)PN_RB * PN_QMAX * 2 * sizeof(double) + 2 * (size_t)h->lda * sizeof(double);
@@ -583,9 +577,11 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
     // so it is opt-in (RGDBEK_PN_SMEM=1)
     if (need <= 200 * 1024 && getenv("RGDBEK_PN_SMEM")) { h->p_dyn = std::max(h->p_dyn, need); pn_smem = 1; }
   }
-  CK(h, cudaFuncSetAttribute(k_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->p_dyn));
-  CK(h, cudaFuncSetAttribute(k_persistent_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->p_dyn));
-  CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persistent, PT, h->p_dyn));
+  const void* kp = h->dense ? (const void*)k_persistent<true> : (const void*)k_persistent<false>;
+  CK(h, cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->p_dyn));
+  const void* kx = h->dense ? (const void*)k_persistent_exact<true> : (const void*)k_persistent_exact<false>;
+  CK(h, cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->p_dyn));
+  CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kp, PT, h->p_dyn));
   if (occ < 1) return set_err(h, RGDBEK_E_CUDA, "persistent kernel cannot be resident (occupancy 0)");
   // CTAs: about one per MB of per-iteration traffic, at most one per SM
   const double bytes = h->dense ? 16.0 * (double)h->m_loc * (double)h->n
@@ -635,7 +631,6 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
   a.greedy = 0;
   a.eta = h->eta;
   a.pn_smem = pn_smem;
-  a.pn_tma = pn_tma;
   // one-sweep register-column pass T measured slower (223 vs 129 us on C2c): opt-in
   a.pt_rows = getenv("RGDBEK_PT_ROWS") ? 1 : 0;
   if (const char* e = getenv("RGDBEK_PHASE_TIMING")) {
@@ -651,12 +646,14 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
 rgdbek_status launch_persistent(rgdbek_ctx* h) {
   if (h->mode == 1) {
     void* args[] = {(void*)&h->pargs, (void*)&h->eargs};
-    CK(h, cudaLaunchCooperativeKernel((const void*)k_persistent_exact, dim3(h->pG), dim3(PT), args,
+    const void* kx = h->dense ? (const void*)k_persistent_exact<true> : (const void*)k_persistent_exact<false>;
+    CK(h, cudaLaunchCooperativeKernel(kx, dim3(h->pG), dim3(PT), args,
                                       h->p_dyn, h->stream));
     return RGDBEK_OK;
   }
   void* args[] = {(void*)&h->pargs};
-  CK(h, cudaLaunchCooperativeKernel((const void*)k_persistent, dim3(h->pG), dim3(PT), args,
+  const void* kp = h->dense ? (const void*)k_persistent<true> : (const void*)k_persistent<false>;
+  CK(h, cudaLaunchCooperativeKernel(kp, dim3(h->pG), dim3(PT), args,
                                     h->p_dyn, h->stream));
   return RGDBEK_OK;
 }
@@ -1267,7 +1264,8 @@ rgdbek_status rgdbek_set_mode(rgdbek_handle h, int32_t mode, double inner_tol, i
     if (h->engine != 0 || h->dist)
       return set_err(h, RGDBEK_E_STATE, "exact-projection mode runs on the single-GPU persistent engine");
     int occ = 0;
-    CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persistent_exact, PT, h->p_dyn));
+    const void* kx = h->dense ? (const void*)k_persistent_exact<true> : (const void*)k_persistent_exact<false>;
+    CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kx, PT, h->p_dyn));
     if (occ < 1) return set_err(h, RGDBEK_E_CUDA, "exact-mode kernel cannot be resident");
     if (!h->eargs.px) {
       TRY(dalloc(h, &h->eargs.px, h->n));
