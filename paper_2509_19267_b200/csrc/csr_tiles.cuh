@@ -10,7 +10,8 @@
 //   * one thread of the group streams the tile's row pointers, values and
 //     column indices into shared memory with cp.async.bulk (TMA bulk copies,
 //     completion on an mbarrier), TBUF tiles ahead of the group, so the
-//     matrix stream is always in flight while the group works;
+//     matrix stream is always in flight while the group works; the last
+//     warp to finish with a buffer refills it (no warp waits for another);
 //   * the group sums each row from shared memory, `vec` lanes per row, with
 //     the gathers in1[c], in2[c] issued four entries at a time; partial sums
 //     are combined by a fixed shuffle tree (deterministic).
@@ -44,7 +45,7 @@ constexpr int TG = 128;              // threads per worker group
 constexpr int TILE_NNZ = RG_TILE_NNZ;    // nonzeros per tile
 constexpr int TILE_ROWS = RG_TILE_ROWS;  // rows per tile
 constexpr int TBUF = RG_TBUF;        // staged tiles per group (one in use, the rest in flight)
-constexpr int TRING = 2 * TBUF;      // mbarriers per group: full[TBUF], empty[TBUF]
+constexpr int TRING = 2 * TBUF;      // ring words per group: full[TBUF] mbarriers, rel[TBUF] counters
 constexpr int PEND = RG_PEND;        // pass-T columns batched for the key epilogue
 
 // One staged tile.  Windows are widened to 16-byte boundaries (bulk-copy
@@ -75,13 +76,13 @@ __device__ __forceinline__ void group_bar(int id) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(TG) : "memory");
 }
 
-// Per-group ring state: TRING mbarriers in static shared memory (so other
-// phases may reuse the TileSmem area as scratch) — full[b] completes when
-// buffer b's bulk copies have landed, empty[b] when the group's TG/32 warps
-// have released it — and the number of tiles this group has consumed so far
-// (identical in all its threads).
+// Per-group ring state in static shared memory (so other phases may reuse the
+// TileSmem area as scratch): full[b], an mbarrier completing when buffer b's
+// bulk copies have landed, and rel[b], the number of the group's warps done
+// with buffer b (the last one refills it); plus the number of tiles this group
+// has consumed so far (identical in all its threads).
 struct TileRing {
-  unsigned long long* full;   // [TRING]: full[0..TBUF), then empty[0..TBUF)
+  unsigned long long* full;   // [TRING]: full[0..TBUF), then rel[0..TBUF)
   unsigned int used;
 };
 
@@ -90,7 +91,7 @@ struct TileRing {
 __device__ __forceinline__ void tile_ring_init(unsigned long long* bars) {
   for (int i = 0; i < TBUF; ++i) {
     mbar_init(&bars[i], 1);
-    mbar_init(&bars[TBUF + i], TG / 32);
+    bars[TBUF + i] = 0ull;                         // release counter of buffer i
   }
 }
 
@@ -184,6 +185,81 @@ __device__ __forceinline__ void tile_flush(const ColKeyEpi* ep, TilePend* pd, in
   }
 }
 
+// One staged tile's rows, (1 << LV) lanes per row: R[r] = ptr[r0 + r],
+// V[q] = val[p0 + q], I[q] = idx[p0 + q] in shared memory.
+struct TileRows {
+  const long long* R;
+  const double* V;
+  const int* I;
+  long long p0;
+  int r0, nr, lane, lw;
+  bool has_b;
+  const double* b;
+  const double* in1;
+  const double* in2;
+  int use2;
+  double* o1;
+  double* o2;
+  const ColKeyEpi* ep;
+  int acc1;
+  TilePend* pend;
+  int npend;
+};
+
+template <int LV>
+__device__ __forceinline__ void tile_rows(const TileRows& t, double& Wp, double& Yp) {
+  constexpr int v = 1 << LV, spw = 32 >> LV;
+  const int sub = t.lane >> LV, sl = t.lane & (v - 1);
+  for (int base = t.lw * spw; base < t.nr; base += (TG / 32) * spw) {   // warp-uniform bounds
+    const int r = base + sub;
+    const bool valid = r < t.nr;
+    double s1 = 0.0, s2 = 0.0;
+    const double bv = t.has_b && valid && sl == 0 ? t.b[t.r0 + r] : 0.0;   // ahead of the gathers
+    if (valid) {
+      int q = (int)(t.R[r] - t.p0) + sl;
+      const int q1 = (int)(t.R[r + 1] - t.p0);
+      // RU entries per lane per round, predicated: one gather round trip
+      // covers a whole row of up to RU * v entries
+      constexpr int RU = RG_RU;
+      for (; q < q1; q += RU * v) {
+        int c[RU];
+        double g1[RU], g2[RU];
+#pragma unroll
+        for (int e = 0; e < RU; ++e) c[e] = q + e * v < q1 ? t.I[q + e * v] : -1;
+#pragma unroll
+        for (int e = 0; e < RU; ++e) {
+          g1[e] = c[e] >= 0 ? t.in1[c[e]] : 0.0;
+          g2[e] = (t.use2 && c[e] >= 0) ? t.in2[c[e]] : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < RU; ++e) {
+          if (c[e] >= 0) {
+            const double a = t.V[q + e * v];
+            s1 = fma(a, g1[e], s1);
+            s2 = fma(a, g2[e], s2);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = v >> 1; o > 0; o >>= 1) {         // fixed shuffle tree (deterministic)
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (valid && sl == 0) {
+      const int row = t.r0 + r;
+      if (t.ep) {
+        t.o1[row] = s1;
+        t.o2[row] = s2;
+        const int e = t.npend + r;
+        t.pend->s1[e] = s1; t.pend->s2[e] = s2; t.pend->row[e] = row;
+      } else {
+        tile_row_out(row, s1, s2, t.has_b, bv, t.o1, t.o2, Wp, Yp, t.acc1);
+      }
+    }
+  }
+}
+
 __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm, TileRing& ring,
                           const long long* __restrict__ ptr, const int* __restrict__ idx,
                           const double* __restrict__ val, const int* __restrict__ tiles,
@@ -207,25 +283,25 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   group_bar(bar_id);
   unsigned long long* full = ring.full;
-  unsigned long long* empty = ring.full + TBUF;
+  unsigned long long* rel = ring.full + TBUF;      // per-buffer count of warps done with it
   if (lt == 0) {
     for (int i = 0; i < cnt && i < TBUF; ++i) {
       const unsigned u = ring.used + i;
-      // buffer reuse across calls: the previous call's last uses were released
-      if (u >= TBUF) mbar_wait(&empty[u % TBUF], (u / TBUF - 1) & 1u);
       tile_issue(sm, u % TBUF, &full[u % TBUF], tile_desc(tb + i * tstep, tiles, tilep),
                  ptr, idx, val);
     }
   }
   const int lane = lt & 31, lw = lt >> 5;
+  const int lvec = __ffs(vec) - 1;                 // vec is a power of two
   const bool has_b = b != nullptr;
   int npend = 0;                                   // pass T: columns awaiting their keys
   for (int i = 0; i < cnt; ++i) {
     const int t = tb + i * tstep;
     const unsigned u = ring.used + i, bi = u % TBUF;
-    // the producer fetches the descriptor of the tile it refills this buffer with
+    // every warp's lane 0 fetches the descriptor of the tile this buffer is
+    // refilled with (the last warp to release the buffer issues the refill)
     TileDesc nd{0, 0, 0, 0};
-    const bool refill = lt == 0 && i + TBUF < cnt;
+    const bool refill = lane == 0 && i + TBUF < cnt;
     if (refill) nd = tile_desc(t + TBUF * tstep, tiles, tilep);
     mbar_wait(&full[bi], (u / TBUF) & 1u);
     const int r0 = (int)sm->desc[bi][0], nr = (int)(sm->desc[bi][1] - sm->desc[bi][0]);
@@ -265,73 +341,39 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
       // lanes per row for this tile: the mean-length choice `vec`, raised so the
       // tile's rows cover the whole group (a tile of few long rows still keeps
       // every thread busy); a power of two <= 32, uniform across the tile
-      int v = vec;
-      while (v < 32 && nr * (2 * v) <= TG) v <<= 1;
-      const int spw = 32 / v, sub = lane / v, sl = lane & (v - 1);
+      int lv = lvec;                               // shifts only: no integer division
+      while (lv < 5 && (nr << (lv + 1)) <= TG) ++lv;
       const TileBuf& B = sm->buf[bi];
-      const long long* R = B.rp + (r0 & 1);        // R[r] = ptr[r0 + r]
-      const double* V = B.val + (p0 & 1);          // V[q] = val[p0 + q]
-      const int* I = B.idx + (p0 & 3);             // I[q] = idx[p0 + q]
-      for (int base = lw * spw; base < nr; base += (TG / 32) * spw) {   // warp-uniform bounds
-        const int r = base + sub;
-        const bool valid = r < nr;
-        double s1 = 0.0, s2 = 0.0;
-        const double bv = has_b && valid && sl == 0 ? b[r0 + r] : 0.0;   // ahead of the gathers
-        if (valid) {
-          int q = (int)(R[r] - p0) + sl;
-          const int q1 = (int)(R[r + 1] - p0);
-          // RU entries per lane per round, predicated: one gather round trip
-          // covers a whole row of up to RU * v entries
-          constexpr int RU = RG_RU;
-          for (; q < q1; q += RU * v) {
-            int c[RU];
-            double g1[RU], g2[RU];
-#pragma unroll
-            for (int e = 0; e < RU; ++e) c[e] = q + e * v < q1 ? I[q + e * v] : -1;
-#pragma unroll
-            for (int e = 0; e < RU; ++e) {
-              g1[e] = c[e] >= 0 ? in1[c[e]] : 0.0;
-              g2[e] = (use2 && c[e] >= 0) ? in2[c[e]] : 0.0;
-            }
-#pragma unroll
-            for (int e = 0; e < RU; ++e) {
-              if (c[e] >= 0) {
-                const double a = V[q + e * v];
-                s1 = fma(a, g1[e], s1);
-                s2 = fma(a, g2[e], s2);
-              }
-            }
-          }
-        }
-        for (int o = v >> 1; o > 0; o >>= 1) {
-          s1 += __shfl_xor_sync(0xffffffffu, s1, o, v);
-          s2 += __shfl_xor_sync(0xffffffffu, s2, o, v);
-        }
-        if (valid && sl == 0) {
-          if (ep) {
-            o1[r0 + r] = s1;
-            o2[r0 + r] = s2;
-            sm->pend.s1[npend + r] = s1; sm->pend.s2[npend + r] = s2; sm->pend.row[npend + r] = r0 + r;
-          } else {
-            tile_row_out(r0 + r, s1, s2, has_b, bv, o1, o2, Wp, Yp, acc1);
-          }
-        }
+      const TileRows tr{B.rp + (r0 & 1), B.val + (p0 & 1), B.idx + (p0 & 3), p0, r0, nr, lane, lw,
+                        has_b, b, in1, in2, use2, o1, o2, ep, acc1, &sm->pend, npend};
+      switch (lv) {                                // lanes per row as a compile-time constant
+        case 0: tile_rows<0>(tr, Wp, Yp); break;
+        case 1: tile_rows<1>(tr, Wp, Yp); break;
+        case 2: tile_rows<2>(tr, Wp, Yp); break;
+        case 3: tile_rows<3>(tr, Wp, Yp); break;
+        case 4: tile_rows<4>(tr, Wp, Yp); break;
+        default: tile_rows<5>(tr, Wp, Yp); break;
       }
     }
     npend += nr;
-    // release buffer bi (each warp once its lanes are done with it); the
-    // warps then run ahead to the next staged tile without a group barrier
+    // release buffer bi: each warp once its lanes are done with it; the last
+    // of the group's warps refills it, so no warp ever waits for another here
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[bi]);
-    if (refill) {
-      mbar_wait(&empty[bi], (u / TBUF) & 1u);
-      tile_issue(sm, bi, &full[bi], nd, ptr, idx, val);
+    if (lane == 0) {
+      __threadfence_block();
+      const unsigned long long done = atomicAdd(&rel[bi], 1ull);
+      if (done == TG / 32 - 1) {
+        __threadfence_block();
+        rel[bi] = 0ull;
+        if (refill) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          tile_issue(sm, bi, &full[bi], nd, ptr, idx, val);
+        }
+      }
     }
   }
-  if (ep) {
-    group_bar(bar_id);
-    tile_flush(ep, &sm->pend, npend, lt, Wp, Yp);
-  }
+  group_bar(bar_id);                               // buffers and pend list free for the next call
+  if (ep) tile_flush(ep, &sm->pend, npend, lt, Wp, Yp);
   ring.used += cnt;
 }
 
