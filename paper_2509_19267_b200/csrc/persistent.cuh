@@ -859,6 +859,13 @@ __device__ void p_zero_side(const PArgs& a, int side) {
   }
 }
 
+#ifndef RG_VEC_PREFETCH
+#define RG_VEC_PREFETCH 1
+#endif
+#ifndef RG_VEC_PREFETCH2
+#define RG_VEC_PREFETCH2 0
+#endif
+
 // ---------------------------------------------------------------------------
 // The persistent kernel.
 // ---------------------------------------------------------------------------
@@ -1040,6 +1047,31 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       double Zp = 0.0, Rp = 0.0;
       long long cnt = 0;
       unsigned long long hs = 0ull;
+#if RG_VEC_PREFETCH2
+      const int stride = G * PT;
+      const int j0 = blockIdx.x * PT + threadIdx.x;
+      double ns = 0.0, nx = 0.0, nv = 0.0, nxs = 0.0;
+      unsigned long long nk = 0ull;
+      if (j0 < n) {
+        ns = a.s[j0]; nk = a.keys_n[j0]; nx = a.x[j0];
+        nv = do_x ? a.v[j0] : 0.0; nxs = has_ref ? a.xstar[j0] : 0.0;
+      }
+      for (int j = j0; j < n; j += stride) {
+        const double sj = ns, vj = nv, xsj = nxs;
+        const unsigned long long kj = nk;
+        double xj = nx;
+        if (j + stride < n) {
+          const int q = j + stride;
+          ns = a.s[q]; nk = a.keys_n[q]; nx = a.x[q];
+          nv = do_x ? a.v[q] : 0.0; nxs = has_ref ? a.xstar[q] : 0.0;
+        }
+        const bool sel = p_selected(&ps, kj, j);
+        a.zeta[j] = sel ? sj : 0.0;
+        if (sel) { Zp += sj * sj; cnt += 1; hs += splitmix64((unsigned long long)j); }
+        if (do_x) { xj = __dadd_rn(xj, __dmul_rn(alpha_x, vj)); a.x[j] = xj; }
+        if (has_ref) { const double d = xj - xsj; Rp += d * d; }
+      }
+#else
       for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) {
         const double sj = a.s[j];
         const bool sel = p_selected(&ps, a.keys_n[j], j);
@@ -1049,6 +1081,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
         if (do_x) { xj = __dadd_rn(xj, __dmul_rn(alpha_x, a.v[j])); a.x[j] = xj; }
         if (has_ref) { const double d = xj - a.xstar[j]; Rp += d * d; }
       }
+#endif
       cnt = warp_sum_ll(cnt);
       hs = warp_sum_u64(hs);
       if ((threadIdx.x & 31) == 0 && (cnt || hs)) {
@@ -1125,12 +1158,33 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     {
       const int doz = kp > 0 && W > 0.0;
       const double az = doz ? __ddiv_rn(Z, W) : 0.0;
+#if RG_VEC_PREFETCH
+      // software-pipelined: the next element's five inputs are in flight while
+      // this element's key (Philox + log + two divisions) is computed
+      const int stride = G * PT;
+      int i0 = blockIdx.x * PT + threadIdx.x;
+      double nz = 0.0, nw = 0.0, nb = 0.0, nax = 0.0, nrho = 0.0;
+      if (i0 < m_loc) {
+        nz = a.z[i0]; nw = doz ? a.w[i0] : 0.0; nb = a.b[i0]; nax = a.ax[i0]; nrho = a.rho[i0];
+      }
+      for (int i = i0; i < m_loc; i += stride) {
+        double zi = nz;
+        const double wi = nw, bi = nb, axi = nax, p = nrho;
+        if (i + stride < m_loc) {
+          const int j = i + stride;
+          nz = a.z[j]; nw = doz ? a.w[j] : 0.0; nb = a.b[j]; nax = a.ax[j]; nrho = a.rho[j];
+        }
+        if (doz) { zi = __dsub_rn(zi, __dmul_rn(az, wi)); a.z[i] = zi; }
+        const double ri = __dsub_rn(__dsub_rn(bi, zi), axi);
+        a.r[i] = ri;
+#else
       for (int i = blockIdx.x * PT + threadIdx.x; i < m_loc; i += G * PT) {
         double zi = a.z[i];
         if (doz) { zi = __dsub_rn(zi, __dmul_rn(az, a.w[i])); a.z[i] = zi; }
         const double ri = __dsub_rn(__dsub_rn(a.b[i], zi), a.ax[i]);
         a.r[i] = ri;
         const double p = a.rho[i];
+#endif
         const double eps = p > 0.0 ? __ddiv_rn(__dmul_rn(ri, ri), p) : 0.0;
         EmaxM = fmax(EmaxM, eps);
         const unsigned long long key = sel_key(eps, (unsigned long long)(a.row0 + i), k, 1u, seed, a.greedy);
@@ -1177,6 +1231,22 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       double Xp = 0.0;
       long long cnt = 0;
       unsigned long long hs = 0ull;
+#if RG_VEC_PREFETCH2
+      const int stride = G * PT;
+      const int i0 = blockIdx.x * PT + threadIdx.x;
+      unsigned long long nk = 0ull;
+      double nr = 0.0;
+      if (i0 < m_loc) { nk = a.keys_m[i0]; nr = a.r[i0]; }
+      for (int i = i0; i < m_loc; i += stride) {
+        const unsigned long long ki = nk;
+        const double ri = nr;
+        if (i + stride < m_loc) { nk = a.keys_m[i + stride]; nr = a.r[i + stride]; }
+        const long long gi = a.row0 + i;
+        const bool sel = p_selected(&ps, ki, gi);
+        a.xi[i] = sel ? ri : 0.0;
+        if (sel) { Xp += ri * ri; cnt += 1; hs += splitmix64((unsigned long long)gi); }
+      }
+#else
       for (int i = blockIdx.x * PT + threadIdx.x; i < m_loc; i += G * PT) {
         const long long gi = a.row0 + i;
         const bool sel = p_selected(&ps, a.keys_m[i], gi);
@@ -1184,6 +1254,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
         a.xi[i] = sel ? ri : 0.0;
         if (sel) { Xp += ri * ri; cnt += 1; hs += splitmix64((unsigned long long)gi); }
       }
+#endif
       cnt = warp_sum_ll(cnt);
       hs = warp_sum_u64(hs);
       if ((threadIdx.x & 31) == 0 && (cnt || hs)) {
