@@ -22,7 +22,10 @@ constexpr int PW = PT / 32;
 constexpr int ZCH = 1024;                 // rows of z / xi staged per chunk (pass T)
 constexpr int PN_RB = 256;                // max rows per batch (dense pass N)
 constexpr int PN_QMAX = 8;                // max column chunks per row (dense pass N)
-constexpr int LOCAL_SEL_MAX = 32768;      // selections over <= this many keys run CTA-locally
+#ifndef RG_LOCAL_SEL_MAX
+#define RG_LOCAL_SEL_MAX 32768
+#endif
+constexpr int LOCAL_SEL_MAX = RG_LOCAL_SEL_MAX;   // selections over <= this many keys run CTA-locally
 
 struct GridBar {
   unsigned int count;
@@ -420,8 +423,13 @@ constexpr int LCAND_CAP = 4096;
 __device__ bool p_sel_local_smem(PSel* ps, const unsigned long long* __restrict__ keys,
                                  long long N, long long idx_base, const unsigned int* gh1,
                                  unsigned int* h, unsigned int* sh_u, long long* sh_l,
-                                 Cand* cl, Cand* fc) {
+                                 Cand* cl, Cand* fc, unsigned long long* pt = nullptr) {
   if (ps->mode != SEL_PENDING) return true;
+  // optional sub-phase timers (RGDBEK_PHASE_TIMING): pt[0..3] += gather, level 2,
+  // level 3, final rank — read by thread 0 of CTA 0 only
+  const bool tim = pt && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long t0 = tim ? gtimer() : 0ull;
+#define SUBT(i) if (tim) { const unsigned long long t1 = gtimer(); pt[i] += t1 - t0; t0 = t1; }
   const unsigned int c1 = __ldcg(gh1 + ps->prefix);
   if (c1 > (unsigned int)LCAND_CAP) return false;
   __shared__ int nc, nf;
@@ -436,6 +444,7 @@ __device__ bool p_sel_local_smem(PSel* ps, const unsigned long long* __restrict_
     }
   }
   __syncthreads();
+  SUBT(0);
   const int cnt = nc < LCAND_CAP ? nc : LCAND_CAP;
   for (int lv = 2; lv <= 3; ++lv) {
     const int sf = lv == 2 ? L1_SHIFT : L2_SHIFT;
@@ -456,6 +465,7 @@ __device__ bool p_sel_local_smem(PSel* ps, const unsigned long long* __restrict_
       ps->below += below;
     }
     __syncthreads();
+    SUBT(lv - 1);
   }
   const unsigned long long pre3 = ps->prefix;
   for (int e = threadIdx.x; e < cnt; e += PT) {
@@ -485,6 +495,8 @@ __device__ bool p_sel_local_smem(PSel* ps, const unsigned long long* __restrict_
   __syncthreads();
   if (threadIdx.x == 0) ps->mode = SEL_THRESH;
   __syncthreads();
+  SUBT(3);
+#undef SUBT
   return true;
 }
 
@@ -1208,7 +1220,8 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     } else if (m_loc <= LOCAL_SEL_MAX) {
       p_sel_level1(&ps, hm, m_loc, kr, sh_u, sh_l);
       if (!p_sel_local_smem(&ps, a.keys_m, m_loc, a.row0, hm, h, sh_u, sh_l,
-                            reinterpret_cast<Cand*>(dyn), reinterpret_cast<Cand*>(dyn) + LCAND_CAP)) {
+                            reinterpret_cast<Cand*>(dyn), reinterpret_cast<Cand*>(dyn) + LCAND_CAP,
+                            a.ptime ? a.ptime + 18 : nullptr)) {
         if (a.ptime && lead) a.ptime[17] += 1;
         p_sel_local(&ps, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
       }

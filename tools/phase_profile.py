@@ -44,6 +44,9 @@ def main():
             out["us_per_iter_total"] = round(sum(t[i] for i in PHASES) / 1e3 / iters, 2)
             if len(t) > 17:
                 out["local_sel_overflows"] = {"col": int(t[16]), "row": int(t[17])}
+            if len(t) > 21:
+                out["rowsel_local_split_us"] = {k: round(t[18 + i] / 1e3 / iters, 2) for i, k in
+                                                enumerate(["gather", "level2", "level3", "rank"])}
         s.close()
     print(json.dumps(out))
 
