@@ -321,6 +321,44 @@ def test_full_size_c3_sampled():
     assert np.linalg.norm(s.z() - o.z) <= 1e-10 * np.linalg.norm(w.b)
 
 
+def test_full_size_c4_sampled():
+    """C4 (1M-pixel Toeplitz blur, 43M nnz) at full size, in bench.py's launch
+    configuration: 3 iterations, blocks identical, x / z within 1e-10."""
+    from workloads import by_name
+    w = by_name("C4")
+    s = _solver(w)
+    o = _oracle(w)
+    s.reset(0)
+    recs = [o.iterate(0) for _ in range(3)]
+    s.step(3)
+    t = s.trace()
+    assert [(r["kp"], r["hash_u"], r["kpp"], r["hash_j"]) for r in t] == \
+           [(r.kp, r.hash_u, r.kpp, r.hash_j) for r in recs]
+    assert np.linalg.norm(s.x() - o.x) <= 1e-10 * np.linalg.norm(o.x)
+    assert np.linalg.norm(s.z() - o.z) <= 1e-10 * np.linalg.norm(w.b)
+
+
+@pytest.mark.parametrize("eta", [0.5, 0.1])
+def test_full_size_c2c_time_to_tolerance(eta):
+    """The headline metric's second half at full size (20000 x 5000): iterations
+    to relative error 1e-6 within +-2 % of the oracle's own count (SURVEY V13
+    quotes 62 at eta = 0.5 and 165 at eta = 0.1 from an independent run)."""
+    from oracle import STOP_REL_ERR
+    from paper_2509_19267_b200 import RGDBEK_CONVERGED
+    from workloads import by_name
+    w = by_name("C2c")
+    w.eta = eta
+    s = _solver(w, stop="rel_err")
+    s.set_reference(w.xstar)
+    res = s.solve(1e-6, 100000, 0)
+    o = _oracle(w)
+    out, iters, rse, rel = o.solve(1e-6, 100000, 0, stop=STOP_REL_ERR, xstar=w.xstar)
+    assert res["outcome"] == RGDBEK_CONVERGED == out
+    assert abs(res["iters"] - iters) <= max(1, int(0.02 * iters)), (res["iters"], iters)
+    assert res["rel_err"] <= 1e-6
+    s.close()
+
+
 @pytest.mark.parametrize("name", ["C2si", "C5t", "C3s"])
 def test_sharded_code_path_world1_nccl(name):
     """The row-sharded (NCCL) code path of the library on one GPU: a world of 1
