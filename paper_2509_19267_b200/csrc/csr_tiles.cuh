@@ -38,6 +38,9 @@ namespace rg {
 #ifndef RG_RU
 #define RG_RU 6
 #endif
+#ifndef RG_REV_N
+#define RG_REV_N 1        // pass N walks the tiles / rows in reverse (L2 reuse after pass T)
+#endif
 #ifndef RG_TILE_BLOCKED
 #define RG_TILE_BLOCKED 0
 #endif
@@ -267,7 +270,8 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
                           const double* in1, const double* in2, int use2,
                           const double* __restrict__ b, double* o1, double* o2,
                           double& Wp, double& Yp,
-                          const ColKeyEpi* ep = nullptr, int acc1 = 0, int vec = 1) {
+                          const ColKeyEpi* ep = nullptr, int acc1 = 0, int vec = 1,
+                          int rev = 0) {
   // default: tiles gid, gid + ngroups, ...: at any moment the groups of the
   // whole GPU stream one contiguous window of the matrix (measured faster on C3
   // than a contiguous run of tiles per group, RG_TILE_BLOCKED=1)
@@ -287,7 +291,8 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
   if (lt == 0) {
     for (int i = 0; i < cnt && i < TBUF; ++i) {
       const unsigned u = ring.used + i;
-      tile_issue(sm, u % TBUF, &full[u % TBUF], tile_desc(tb + i * tstep, tiles, tilep),
+      const int ti = tb + i * tstep;
+      tile_issue(sm, u % TBUF, &full[u % TBUF], tile_desc(rev ? ntiles - 1 - ti : ti, tiles, tilep),
                  ptr, idx, val);
     }
   }
@@ -296,13 +301,16 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
   const bool has_b = b != nullptr;
   int npend = 0;                                   // pass T: columns awaiting their keys
   for (int i = 0; i < cnt; ++i) {
-    const int t = tb + i * tstep;
+    const int t = tb + i * tstep;                  // (reversed below when rev)
     const unsigned u = ring.used + i, bi = u % TBUF;
     // every warp's lane 0 fetches the descriptor of the tile this buffer is
     // refilled with (the last warp to release the buffer issues the refill)
     TileDesc nd{0, 0, 0, 0};
     const bool refill = lane == 0 && i + TBUF < cnt;
-    if (refill) nd = tile_desc(t + TBUF * tstep, tiles, tilep);
+    if (refill) {
+      const int tn = t + TBUF * tstep;
+      nd = tile_desc(rev ? ntiles - 1 - tn : tn, tiles, tilep);
+    }
     mbar_wait(&full[bi], (u / TBUF) & 1u);
     const int r0 = (int)sm->desc[bi][0], nr = (int)(sm->desc[bi][1] - sm->desc[bi][0]);
     const long long p0 = sm->desc[bi][2], p1 = sm->desc[bi][3];

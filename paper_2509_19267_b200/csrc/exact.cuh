@@ -97,7 +97,7 @@ __device__ void ex_passN(const PArgs& a, TileRing& ring, const double* in1, cons
     csr_tiles(blockIdx.x * (PT / TG) + g, gridDim.x * (PT / TG), threadIdx.x % TG, 1 + g,
               reinterpret_cast<TileSmem*>(dyn) + g, ring, a.rp, a.ci, a.cv, a.tilesN, a.tilepN,
               a.ntilesN, in1,
-              in2, 1, bvec, o1, o2, Wp, Yp, nullptr, bvec ? 0 : 1, a.vecN);
+              in2, 1, bvec, o1, o2, Wp, Yp, nullptr, bvec ? 0 : 1, a.vecN, RG_REV_N);
   }
 }
 

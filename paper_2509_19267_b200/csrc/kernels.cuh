@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(NT) k_csr_tiles(const long long* __restrict__ 
   double Wp = 0.0, Yp = 0.0;
   csr_tiles(blockIdx.x * GPB + g, gridDim.x * GPB, threadIdx.x % TG, 1 + g, sm, ring, ptr, idx,
             val, tiles, tilep, ntiles, in1, in2, use2, MODE == 0 ? b : nullptr, o1, o2, Wp, Yp,
-            nullptr, 0, vec);
+            nullptr, 0, vec, MODE == 0 ? RG_REV_N : 0);
   if (MODE == 1) return;
   const double Wb = block_sum<NT>(Wp, sh);
   const double Yb = block_sum<NT>(Yp, sh);

@@ -20,6 +20,12 @@ namespace rg {
 constexpr int PT = 1024;                  // threads per persistent CTA
 constexpr int PW = PT / 32;
 constexpr int ZCH = 1024;                 // rows of z / xi staged per chunk (pass T)
+#ifndef RG_VEC_PREFETCH
+#define RG_VEC_PREFETCH 1
+#endif
+#ifndef RG_VEC_PREFETCH2
+#define RG_VEC_PREFETCH2 0
+#endif
 constexpr int PN_RB = 256;                // max rows per batch (dense pass N)
 constexpr int PN_QMAX = 8;                // max column chunks per row (dense pass N)
 #ifndef RG_LOCAL_SEL_MAX
@@ -726,11 +732,17 @@ __device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp
   }
   const int nbatch = (re - rb + PN_RB - 1) / PN_RB;             // evenly sized batches
   const int per = nbatch ? (re - rb + nbatch - 1) / nbatch : 0;
-  for (int r0 = rb; r0 < re; r0 += per) {
+  // rows bottom-up (batches and row pairs in reverse): pass T just streamed this
+  // CTA's rows top-down, so the rows it read last are still in L2 when pass N
+  // starts; the next pass T (top-down) then meets the rows pass N read last
+  for (int bt = nbatch - 1; bt >= 0; --bt) {
+    const int r0 = rb + (RG_REV_N ? bt : nbatch - 1 - bt) * per;
     const int rows = min(per, re - r0);
-    const int units = ((rows + 1) >> 1) * Q;                     // 2 rows x 1 chunk per unit
+    const int npairs = (rows + 1) >> 1;
+    const int units = npairs * Q;                                // 2 rows x 1 chunk per unit
     for (int u = wid; u < units; u += PW) {
-      const int rp = u / Q, q = u - rp * Q;
+      const int up = u / Q, q = u - up * Q;
+      const int rp = RG_REV_N ? npairs - 1 - up : up;
       const int rr = 2 * rp;
       const bool two = rr + 1 < rows;
       const int c0 = q * CH, c1 = min(n, c0 + CH);
@@ -871,12 +883,6 @@ __device__ void p_zero_side(const PArgs& a, int side) {
   }
 }
 
-#ifndef RG_VEC_PREFETCH
-#define RG_VEC_PREFETCH 1
-#endif
-#ifndef RG_VEC_PREFETCH2
-#define RG_VEC_PREFETCH2 0
-#endif
 
 // ---------------------------------------------------------------------------
 // The persistent kernel.
@@ -1126,7 +1132,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
         csr_tiles(blockIdx.x * (PT / TG) + g, G * (PT / TG), threadIdx.x % TG, 1 + g,
                   reinterpret_cast<TileSmem*>(dyn) + g, tring, a.rp, a.ci, a.cv, a.tilesN,
                   a.tilepN, a.ntilesN,
-                  a.zeta, a.x, 1, a.b, a.w, a.ax, Wp, Yp, nullptr, 0, a.vecN);
+                  a.zeta, a.x, 1, a.b, a.w, a.ax, Wp, Yp, nullptr, 0, a.vecN, RG_REV_N);
       }
       const double wb = pblock_sum(Wp, sh);
       const double yb = pblock_sum(Yp, sh);
