@@ -165,6 +165,20 @@ rgdbek_status rgdbek_set_mode(rgdbek_handle h, int32_t mode, double inner_tol, i
  * (no sampling; block sizes vary).  Combine with rgdbek_set_mode(1) for GDBEK's
  * pseudoinverse updates (eq:updateGDBEK).  Needs the single-GPU persistent engine. */
 rgdbek_status rgdbek_set_selection(rgdbek_handle h, int32_t selection);
+
+/* The paper's parallel Algorithm 2 (alg:rgdbek_bsas) on ONE
+ * GPU with `processes` logical processes P in [1, 8]: the rows are split into P
+ * contiguous blocks [floor(m p/P), floor(m (p+1)/P)); every iteration samples one global
+ * column set U from A^T z, lets each process take its own first-Krylov
+ * z-step on its rows and sample round(eta d_p) of its own rows,
+ * and applies the lazily averaged x-update x += (1/P) sum_p (X_p/V_p) (A^(p))^T xi_p
+ * — the pseudoinverse-free reading R28 of DESIGN.md.  P = 1 is Algorithm 1.
+ * processes = 0 returns to Algorithm 1.  Needs a dense A on the single-GPU persistent
+ * engine, the pseudoinverse-free update and random selection (RGDBEK_E_STATE otherwise),
+ * and at most 32768 rows per process (RGDBEK_E_ARG).  The persistent grid is rounded
+ * down to a multiple of P (each process is a run of G/P CTAs).  Traces report the sums
+ * over processes of Z_p, W_p, X_p, V_p and |J| = sum_p |J_p|. */
+rgdbek_status rgdbek_set_lazy(rgdbek_handle h, int32_t processes);
 rgdbek_status rgdbek_set_reference(rgdbek_handle h, const double* xstar /* n values */);
 
 rgdbek_status rgdbek_get_x(rgdbek_handle h, double* out_n);

@@ -154,6 +154,11 @@ class Solver:
         r = {"random": 0, "greedy": 1}[rule] if isinstance(rule, str) else int(rule)
         N.rgdbek_set_selection(self._h, r)
 
+    def set_lazy(self, processes):
+        """The paper's parallel Algorithm 2 with `processes` logical row processes
+        (lazily averaged x-update); 0 returns to Algorithm 1."""
+        N.rgdbek_set_lazy(self._h, int(processes))
+
     def passes(self):
         """Full passes over A since the last reset (persistent engine)."""
         return N.rgdbek_get_counters(self._h)

@@ -23,7 +23,7 @@ EXPORTED = [
     "rgdbek_get_x", "rgdbek_get_z", "rgdbek_get_blocks", "rgdbek_get_trace", "rgdbek_set_state",
     "rgdbek_launch_kernel", "rgdbek_launches_per_iteration", "rgdbek_stream",
     "rgdbek_phase_times", "rgdbek_engine_info", "rgdbek_set_mode", "rgdbek_get_counters",
-    "rgdbek_set_selection",
+    "rgdbek_set_selection", "rgdbek_set_lazy",
     "rgdbek_nccl_unique_id", "rgdbek_nccl_comm_init", "rgdbek_nccl_comm_destroy",
     "rgdbek_last_error", "rgdbek_destroy",
 ]
@@ -98,6 +98,7 @@ def load(path=None):
         "rgdbek_set_mode": (C.c_int, [H, C.c_int32, C.c_double, C.c_int32]),
         "rgdbek_get_counters": (C.c_int, [H, C.POINTER(C.c_int64)]),
         "rgdbek_set_selection": (C.c_int, [H, C.c_int32]),
+        "rgdbek_set_lazy": (C.c_int, [H, C.c_int32]),
         "rgdbek_nccl_unique_id": (C.c_int, [P]),
         "rgdbek_nccl_comm_init": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, P,
                                             C.c_int32]),
@@ -226,6 +227,10 @@ def rgdbek_set_mode(h, mode, inner_tol=1e-12, inner_max=50):
 
 def rgdbek_set_selection(h, selection):
     check(load().rgdbek_set_selection(h, int(selection)), h)
+
+
+def rgdbek_set_lazy(h, processes):
+    check(load().rgdbek_set_lazy(h, int(processes)), h)
 
 
 def rgdbek_get_counters(h):

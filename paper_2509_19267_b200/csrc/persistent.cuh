@@ -41,6 +41,7 @@ struct GridBar {
 };
 
 enum : int { SL_V = 0, SL_Z, SL_R, SL_W, SL_Y, SL_X, SL_MAXN, SL_MAXM, SL_NUM };
+constexpr int LZ_MAX = 8;                  // Algorithm 2: at most 8 logical processes
 
 struct PArgs {
   int dense, m_loc, n, vecN, vecT, Q, CH;
@@ -68,6 +69,15 @@ struct PArgs {
   double eta;
   int pn_smem;                      // dense pass N: zeta / x staged in shared memory
   int pt_rows;                      // dense pass T: one-sweep register-column form
+  // Algorithm 2 (lazy averaging, P logical row processes; k_persistent<true, true>)
+  int lzP, lzGp;                    // processes; CTAs per process (G = lzP * lzGp)
+  long long lz_r0[LZ_MAX + 1];      // process row ranges [lz_r0[p], lz_r0[p + 1])
+  long long lz_kr[LZ_MAX];          // per-process row block sizes round(eta d_p)
+  double* lz_g;                     // [P][n] (A^(p))^T z^(p)
+  double* lz_v;                     // [P][n] (A^(p))^T xi^(p)
+  double* lz_zeta;                  // [P][n] zeta_p = g_p on U
+  unsigned int* lz_hist;            // [P][NBINS] level-1 histograms of the row keys
+  double* lz_slots;                 // [2 P][G]: per-CTA partials of V_p, Z_p
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -124,6 +134,25 @@ __device__ __forceinline__ double pblock_sum(double v, double* sh) {
 }
 
 // Sum over the G per-CTA partials of one slot (identical in every CTA).
+// Algorithm 2: P sums of per-CTA partials, out[p] = sum_c base[p * pstride + c]
+// for c in [p * cstart, p * cstart + count); warp p sums, lanes strided, fixed
+// tree (deterministic).  Per-process sums over the process's own CTAs use
+// (pstride 0, cstart Gp, count Gp); sums over every CTA of a per-process
+// quantity use (pstride G, cstart 0, count G).  out[] is shared memory, valid
+// for every thread on return.
+__device__ __forceinline__ void lz_sums(const double* base, int pstride, int cstart, int count,
+                                        int P, double* out) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (w < P) {
+    double t = 0.0;
+    const double* q = base + (long long)w * pstride + (long long)w * cstart;
+    for (int c = l; c < count; c += 32) t += __ldcg(q + c);
+    t = warp_sum(t);
+    if (l == 0) out[w] = t;
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ double slot_sum(const double* bpart, int slot, double* sh) {
   double t = 0.0;
   for (int i = threadIdx.x; i < (int)gridDim.x; i += PT) t += __ldcg(bpart + slot * gridDim.x + i);
@@ -890,7 +919,7 @@ __device__ void p_zero_side(const PArgs& a, int side) {
 // DENSE selects the pass kernels at compile time: each instantiation carries
 // only its own pass code, so the register allocation (64 per thread at 1024
 // threads) is not shared between the dense and the sparse paths.
-template <bool DENSE>
+template <bool DENSE, bool LAZY = false>
 __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
   __shared__ __align__(16) unsigned int h[NBINS];
   __shared__ __align__(8) unsigned long long tbar[(PT / TG) * TRING];
@@ -898,6 +927,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
   __shared__ unsigned int sh_u[4];
   __shared__ long long sh_l[40];
   __shared__ PSel ps;
+  __shared__ double lzs[4][LZ_MAX];      // Algorithm 2: per-process V, X, Z, W
   extern __shared__ __align__(16) double dyn[];
   TileRing tring{tbar + (threadIdx.x / TG) * TRING, 0u};
   if (!DENSE) tile_rings_init(tbar);
@@ -943,6 +973,9 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       grid_sync(a.bar, bgen);
       PH(1);
       p_zero_side(a, 1);                        // m-side buffers: consumed in P9..P12
+      if constexpr (LAZY) {
+        for (int i = blockIdx.x * PT + threadIdx.x; i < a.lzP * NBINS; i += G * PT) a.lz_hist[i] = 0u;
+      }
 
       // ===== P2 (dense): s, v = sum of the CTA partials; V; keys; level-1 histogram =====
       for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
@@ -951,7 +984,45 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       // partials p = g, g + 16, ... of column c0 + chunk + c (coalesced across c),
       // then the 16 group sums are added in group order (deterministic) and one
       // thread per column makes its key — all columns of a CTA in parallel.
-      {
+      if constexpr (LAZY) {
+        // Algorithm 2: g_p = (A^(p))^T z^(p), v_p = (A^(p))^T xi^(p) from the CTA
+        // partials of process p (its CTAs, in order); s = sum_p g_p (process order)
+        const int cpb = (n + G - 1) / G;
+        const int c0 = min(n, blockIdx.x * cpb), c1 = min(n, c0 + cpb);
+        const int nc = c1 - c0, P = a.lzP, Gp = a.lzGp;
+        double* gS = dyn;                         // [P][cpb]
+        double* vS = dyn + P * cpb;               // [P][cpb]
+        for (int it = threadIdx.x; it < P * nc; it += PT) {
+          const int pp = it / nc, jl = it - pp * nc, j = c0 + jl;
+          double gs = 0.0, vs = 0.0;
+          for (int c = pp * Gp; c < (pp + 1) * Gp; ++c) {
+            const double* q = a.part + (long long)c * 2 * n + j;
+            gs += __ldcg(q);
+            if (pending) vs += __ldcg(q + n);
+          }
+          gS[pp * cpb + jl] = gs;
+          vS[pp * cpb + jl] = vs;
+          a.lz_g[(long long)pp * n + j] = gs;
+          a.lz_v[(long long)pp * n + j] = vs;
+        }
+        __syncthreads();
+        if (threadIdx.x < nc) {
+          const int jl = threadIdx.x, j = c0 + jl;
+          double ts = 0.0;
+          for (int pp = 0; pp < P; ++pp) ts += gS[pp * cpb + jl];
+          a.s[j] = ts;
+          const double gm = a.gamma[j];
+          const double eps = gm > 0.0 ? __ddiv_rn(__dmul_rn(ts, ts), gm) : 0.0;
+          const unsigned long long key = sel_key(eps, (unsigned long long)j, k, 0u, seed, 0);
+          a.keys_n[j] = key;
+          atomicAdd(&h[key >> L1_SHIFT], 1u);
+        } else if (threadIdx.x >= PT - P) {     // V_p partial of this CTA's columns
+          const int pp = threadIdx.x - (PT - P);
+          double t = 0.0;
+          for (int jl = 0; jl < nc; ++jl) t += vS[pp * cpb + jl] * vS[pp * cpb + jl];
+          a.lz_slots[(long long)pp * G + blockIdx.x] = t;
+        }
+      } else {
         constexpr int CW = 64, NG = PT / CW;
         double* red = dyn;                        // [2][NG][CW]
         const int cpb = (n + G - 1) / G;
@@ -1030,7 +1101,17 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     }
 
     // ===== P3: V, alpha_x; level-1 bucket (U); level-2 scan =====
-    const double V = slot_sum(bp, SL_V, sh);
+    double V;
+    if constexpr (LAZY) {
+      // per-process V_p (over every CTA's columns) and X_p (the process's rows,
+      // last iteration's P11 partials); V = sum_p V_p for the trace
+      lz_sums(a.lz_slots, G, 0, G, a.lzP, lzs[0]);
+      lz_sums(bp + SL_X * G, 0, a.lzGp, a.lzGp, a.lzP, lzs[1]);
+      V = 0.0;
+      for (int pp = 0; pp < a.lzP; ++pp) V += lzs[0][pp];
+    } else {
+      V = slot_sum(bp, SL_V, sh);
+    }
     const int do_x = pending && kpp_prev > 0 && V > 0.0;
     const double alpha_x = do_x ? __ddiv_rn(X, V) : 0.0;
     if (lead && pending) {
@@ -1061,7 +1142,47 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       p_sel_level3(&ps, hn + 2 * NBINS, cn, a.ncand, a.keys_n, n, 0, h, sh_u, sh_l);
     }
     // ===== P5: zeta, Z, |U|, hash; x_k = x_{k-1} + alpha_x v =====
-    {
+    if constexpr (LAZY) {
+      // Algorithm 2: zeta_p = g_p on U (every process), Z_p partials; the lazily
+      // averaged x_k = x_{k-1} + (sum_p (X_p / V_p) v_p) / P
+      const int P = a.lzP;
+      double Zl[LZ_MAX];
+      for (int pp = 0; pp < LZ_MAX; ++pp) Zl[pp] = 0.0;
+      double Rp = 0.0;
+      long long cnt = 0;
+      unsigned long long hs = 0ull;
+      for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) {
+        const bool sel = p_selected(&ps, a.keys_n[j], j);
+        double t = 0.0;
+#pragma unroll
+        for (int pp = 0; pp < LZ_MAX; ++pp) {
+          if (pp < P) {
+            const double g = a.lz_g[(long long)pp * n + j];
+            a.lz_zeta[(long long)pp * n + j] = sel ? g : 0.0;
+            if (sel) Zl[pp] += g * g;
+            const double Xq = lzs[1][pp], Vq = lzs[0][pp];
+            if (pending && Xq > 0.0 && Vq > 0.0)
+              t = __dadd_rn(t, __dmul_rn(__ddiv_rn(Xq, Vq), a.lz_v[(long long)pp * n + j]));
+          }
+        }
+        if (sel) { cnt += 1; hs += splitmix64((unsigned long long)j); }
+        double xj = a.x[j];
+        if (pending) { xj = __dadd_rn(xj, __ddiv_rn(t, (double)P)); a.x[j] = xj; }
+        if (has_ref) { const double d = xj - a.xstar[j]; Rp += d * d; }
+      }
+      cnt = warp_sum_ll(cnt);
+      hs = warp_sum_u64(hs);
+      if ((threadIdx.x & 31) == 0 && (cnt || hs)) {
+        atomicAdd(&a.acc[0], (unsigned long long)cnt);
+        atomicAdd(&a.acc[1], hs);
+      }
+      for (int pp = 0; pp < P; ++pp) {
+        const double zb = pblock_sum(Zl[pp], sh);
+        if (threadIdx.x == 0) a.lz_slots[(long long)(P + pp) * G + blockIdx.x] = zb;
+      }
+      const double rb = pblock_sum(Rp, sh);
+      if (threadIdx.x == 0) { bp[SL_Z * G + blockIdx.x] = 0.0; bp[SL_R * G + blockIdx.x] = rb; }
+    } else {
       double Zp = 0.0, Rp = 0.0;
       long long cnt = 0;
       unsigned long long hs = 0ull;
@@ -1115,7 +1236,14 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     PH(5);
 
     // ===== P6: Z, |U|; pass N (w = A zeta, A x_k) with W / ||b - Ax||^2 partials =====
-    const double Z = slot_sum(bp, SL_Z, sh);
+    double Z;
+    if constexpr (LAZY) {
+      lz_sums(a.lz_slots + (long long)a.lzP * G, G, 0, G, a.lzP, lzs[2]);   // Z_p
+      Z = 0.0;
+      for (int pp = 0; pp < a.lzP; ++pp) Z += lzs[2][pp];
+    } else {
+      Z = slot_sum(bp, SL_Z, sh);
+    }
     const double relerr2 = slot_sum(bp, SL_R, sh);
     const long long kp = (long long)__ldcg(&a.acc[0]);
     const unsigned long long hashU = __ldcg(&a.acc[1]);
@@ -1125,7 +1253,9 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     }
     {
       double Wp = 0.0, Yp = 0.0;
-      if constexpr (DENSE) {
+      if constexpr (LAZY) {                       // w = A^(p) zeta_p on this CTA's process
+        p_dense_passN(a, dyn, Wp, Yp, a.lz_zeta + (long long)(blockIdx.x / a.lzGp) * n);
+      } else if constexpr (DENSE) {
         p_dense_passN(a, dyn, Wp, Yp);
       } else {
         const int g = threadIdx.x / TG;
@@ -1142,7 +1272,14 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     PH(6);
 
     // ===== P8: stop test on x_k; z_{k+1}, r, row scores and keys, level-1 histogram =====
-    const double W = slot_sum(bp, SL_W, sh);
+    double W;
+    if constexpr (LAZY) {                         // W_p over the process's own CTAs
+      lz_sums(bp + SL_W * G, 0, a.lzGp, a.lzGp, a.lzP, lzs[3]);
+      W = 0.0;
+      for (int pp = 0; pp < a.lzP; ++pp) W += lzs[3][pp];
+    } else {
+      W = slot_sum(bp, SL_W, sh);
+    }
     const double Y = slot_sum(bp, SL_Y, sh);
     {
       const double rse = Y / bnorm2;
@@ -1174,21 +1311,28 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     __syncthreads();
     double EmaxM = 0.0;
     {
-      const int doz = kp > 0 && W > 0.0;
-      const double az = doz ? __ddiv_rn(Z, W) : 0.0;
+      // Algorithm 2: the local z-step of this CTA's process, alpha = Z_p / W_p
+      const int lzp = LAZY ? (int)(blockIdx.x / a.lzGp) : 0;
+      const double Zs = LAZY ? lzs[2][lzp] : Z, Ws = LAZY ? lzs[3][lzp] : W;
+      const int doz = kp > 0 && Ws > 0.0;
+      const double az = doz ? __ddiv_rn(Zs, Ws) : 0.0;
+      // rows of this sweep: grid-stride over all rows, or (Algorithm 2) this
+      // CTA's own contiguous rows, which lie in its process
+      const int m_end = LAZY ? (int)((long long)m_loc * (blockIdx.x + 1) / G) : m_loc;
 #if RG_VEC_PREFETCH
       // software-pipelined: the next element's five inputs are in flight while
       // this element's key (Philox + log + two divisions) is computed
-      const int stride = G * PT;
-      int i0 = blockIdx.x * PT + threadIdx.x;
+      const int stride = LAZY ? PT : G * PT;
+      int i0 = LAZY ? (int)((long long)m_loc * blockIdx.x / G) + threadIdx.x
+                    : blockIdx.x * PT + threadIdx.x;
       double nz = 0.0, nw = 0.0, nb = 0.0, nax = 0.0, nrho = 0.0;
-      if (i0 < m_loc) {
+      if (i0 < m_end) {
         nz = a.z[i0]; nw = doz ? a.w[i0] : 0.0; nb = a.b[i0]; nax = a.ax[i0]; nrho = a.rho[i0];
       }
-      for (int i = i0; i < m_loc; i += stride) {
+      for (int i = i0; i < m_end; i += stride) {
         double zi = nz;
         const double wi = nw, bi = nb, axi = nax, p = nrho;
-        if (i + stride < m_loc) {
+        if (i + stride < m_end) {
           const int j = i + stride;
           nz = a.z[j]; nw = doz ? a.w[j] : 0.0; nb = a.b[j]; nax = a.ax[j]; nrho = a.rho[j];
         }
@@ -1196,6 +1340,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
         const double ri = __dsub_rn(__dsub_rn(bi, zi), axi);
         a.r[i] = ri;
 #else
+      static_assert(!LAZY || RG_VEC_PREFETCH, "Algorithm 2 uses the pipelined row sweep");
       for (int i = blockIdx.x * PT + threadIdx.x; i < m_loc; i += G * PT) {
         double zi = a.z[i];
         if (doz) { zi = __dsub_rn(zi, __dmul_rn(az, a.w[i])); a.z[i] = zi; }
@@ -1211,7 +1356,11 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       }
     }
     __syncthreads();
-    flush_hist<PT>(h, hm, NBINS);
+    if constexpr (LAZY) {
+      flush_hist<PT>(h, a.lz_hist + (long long)(blockIdx.x / a.lzGp) * NBINS, NBINS);
+    } else {
+      flush_hist<PT>(h, hm, NBINS);
+    }
     {
       const double eb = pblock_max(EmaxM, sh);
       if (threadIdx.x == 0) bp[SL_MAXM * G + blockIdx.x] = eb;
@@ -1221,7 +1370,17 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     PH(7);
 
     // ===== P9: level-1 bucket (J); level-2 scan =====
-    if (a.greedy) {
+    if constexpr (LAZY) {
+      // Algorithm 2: each process samples round(eta d_p) of its own rows;
+      // every CTA resolves its process's selection locally (d_p <= LOCAL_SEL_MAX)
+      const int pp = (int)(blockIdx.x / a.lzGp);
+      const long long r0p = a.lz_r0[pp], dp = a.lz_r0[pp + 1] - r0p;
+      const unsigned int* hp = a.lz_hist + (long long)pp * NBINS;
+      p_sel_level1(&ps, hp, dp, a.lz_kr[pp], sh_u, sh_l);
+      if (!p_sel_local_smem(&ps, a.keys_m + r0p, dp, a.row0 + r0p, hp, h, sh_u, sh_l,
+                            reinterpret_cast<Cand*>(dyn), reinterpret_cast<Cand*>(dyn) + LCAND_CAP))
+        p_sel_local(&ps, a.keys_m + r0p, dp, a.row0 + r0p, h, sh_u, sh_l);
+    } else if (a.greedy) {
       p_sel_greedy(&ps, slot_max(bp, SL_MAXM, sh), a.eta);
     } else if (m_loc <= LOCAL_SEL_MAX) {
       p_sel_level1(&ps, hm, m_loc, kr, sh_u, sh_l);
@@ -1266,7 +1425,10 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
         if (sel) { Xp += ri * ri; cnt += 1; hs += splitmix64((unsigned long long)gi); }
       }
 #else
-      for (int i = blockIdx.x * PT + threadIdx.x; i < m_loc; i += G * PT) {
+      const int i_beg = LAZY ? (int)((long long)m_loc * blockIdx.x / G) + threadIdx.x
+                             : blockIdx.x * PT + threadIdx.x;
+      const int i_end = LAZY ? (int)((long long)m_loc * (blockIdx.x + 1) / G) : m_loc;
+      for (int i = i_beg; i < i_end; i += (LAZY ? PT : G * PT)) {
         const long long gi = a.row0 + i;
         const bool sel = p_selected(&ps, a.keys_m[i], gi);
         const double ri = a.r[i];
@@ -1291,7 +1453,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     const long long kpp = (long long)__ldcg(&a.acc[2]);
     const unsigned long long hashJ = __ldcg(&a.acc[3]);
     if (lead) {
-      if (!a.greedy && kpp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 2;
+      if (!a.greedy && !LAZY && kpp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 2;
       if (TraceRec* t = trace_at(tr, st, k)) { t->kpp = kpp; t->hash_j = hashJ; t->X = X; }
     }
     kp_prev = kp;

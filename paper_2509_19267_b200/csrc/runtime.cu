@@ -73,6 +73,8 @@ struct rgdbek_ctx {
   size_t p_dyn = 0;                     // persistent: dynamic smem bytes
   bool graph_built = false;             // graph engine captured (lazily for engine 0)
   size_t l2_window = 0;                 // bytes of A marked L2-persisting on the stream
+  int lazyP = 0;                        // Algorithm 2 logical processes (0 = Algorithm 1)
+  int pG_base = 0;                      // persistent grid before Algorithm 2's rounding
   PArgs pargs;                          // persistent: kernel arguments
   unsigned int* phist = nullptr;        // persistent: [2][3][NBINS]
   Cand* pcand = nullptr;                // persistent: [2][CAND_CAP]
@@ -656,7 +658,8 @@ rgdbek_status launch_persistent(rgdbek_ctx* h) {
     return RGDBEK_OK;
   }
   void* args[] = {(void*)&h->pargs};
-  const void* kp = h->dense ? (const void*)k_persistent<true> : (const void*)k_persistent<false>;
+  const void* kp = h->lazyP ? (const void*)k_persistent<true, true>
+                 : h->dense ? (const void*)k_persistent<true> : (const void*)k_persistent<false>;
   CK(h, cudaLaunchCooperativeKernel(kp, dim3(h->pG), dim3(PT), args,
                                     h->p_dyn, h->stream));
   return RGDBEK_OK;
@@ -1302,6 +1305,8 @@ rgdbek_status rgdbek_phase_times(rgdbek_handle h, double* out_ns, int32_t max_ph
 rgdbek_status rgdbek_set_mode(rgdbek_handle h, int32_t mode, double inner_tol, int32_t inner_max) {
   TRY(ensure_usable(h));
   if (mode < 0 || mode > 1) return set_err(h, RGDBEK_E_ARG, "unknown update mode %d", mode);
+  if (mode == 1 && h->lazyP)
+    return set_err(h, RGDBEK_E_STATE, "Algorithm 2 (set_lazy) runs the pseudoinverse-free update only");
   if (mode == 1) {
     if (!(inner_tol > 0.0 && inner_tol < 1.0) || inner_max < 1)
       return set_err(h, RGDBEK_E_ARG, "exact mode needs 0 < inner_tol < 1 and inner_max >= 1");
@@ -1327,7 +1332,65 @@ rgdbek_status rgdbek_set_selection(rgdbek_handle h, int32_t selection) {
   if (selection < 0 || selection > 1) return set_err(h, RGDBEK_E_ARG, "unknown selection rule %d", selection);
   if (selection == 1 && (h->engine != 0 || h->dist))
     return set_err(h, RGDBEK_E_STATE, "greedy selection runs on the single-GPU persistent engine");
+  if (selection == 1 && h->lazyP)
+    return set_err(h, RGDBEK_E_STATE, "Algorithm 2 (set_lazy) samples its blocks (random selection only)");
   h->pargs.greedy = selection;
+  return RGDBEK_OK;
+}
+
+// Algorithm 2 with P logical processes = contiguous row blocks
+// (reading R28).  Each process is a contiguous run of G/P CTAs of the dense
+// persistent kernel, so its row block is [floor(m p / P), floor(m (p+1) / P)).
+rgdbek_status rgdbek_set_lazy(rgdbek_handle h, int32_t processes) {
+  TRY(ensure_usable(h));
+  if (processes < 0 || processes > LZ_MAX)
+    return set_err(h, RGDBEK_E_ARG, "processes must lie in [0, %d]", LZ_MAX);
+  if (processes == 0) {                  // back to Algorithm 1
+    h->lazyP = 0;
+    if (h->pG_base) h->pG = h->pG_base;
+    return RGDBEK_OK;
+  }
+  if (!h->dense || h->engine != 0 || h->dist)
+    return set_err(h, RGDBEK_E_STATE, "Algorithm 2 runs on the single-GPU persistent engine, dense A");
+  if (h->mode != 0 || h->pargs.greedy)
+    return set_err(h, RGDBEK_E_STATE, "Algorithm 2 needs the pseudoinverse-free update and random selection");
+  const int P = processes;
+  if (P > h->m_loc) return set_err(h, RGDBEK_E_ARG, "more processes (%d) than rows", P);
+  if (!h->pG_base) h->pG_base = h->pG;
+  const int G = (h->pG_base / P) * P;
+  if (G < P) return set_err(h, RGDBEK_E_ARG, "persistent grid of %d CTAs < %d processes", h->pG_base, P);
+  const long long cpb = (h->n + G - 1) / G;
+  if ((size_t)(2 * P * cpb) * sizeof(double) > h->p_dyn)
+    return set_err(h, RGDBEK_E_ARG, "Algorithm 2: n / G too large for the column-sum staging");
+  PArgs& a = h->pargs;
+  for (int p = 0; p <= P; ++p) {
+    // process p = CTAs [p G/P, (p+1) G/P): its rows start at floor(m_loc * (p G/P) / G)
+    a.lz_r0[p] = (long long)h->m_loc * (p * (G / P)) / G;
+  }
+  for (int p = 0; p < P; ++p) {
+    const long long d = a.lz_r0[p + 1] - a.lz_r0[p];
+    if (d > LOCAL_SEL_MAX)
+      return set_err(h, RGDBEK_E_ARG, "Algorithm 2: %lld rows per process > %d", d, LOCAL_SEL_MAX);
+    a.lz_kr[p] = std::max(1LL, (long long)std::floor(h->eta * (double)d + 0.5));
+  }
+  if (!a.lz_g || h->lazyP < P) {          // buffers for up to P processes
+    TRY(dalloc(h, &a.lz_g, (size_t)P * h->n));
+    TRY(dalloc(h, &a.lz_v, (size_t)P * h->n));
+    TRY(dalloc(h, &a.lz_zeta, (size_t)P * h->n));
+    TRY(dalloc(h, &a.lz_hist, (size_t)P * NBINS));
+    TRY(dalloc(h, &a.lz_slots, (size_t)2 * P * MAXBLK));
+    CK(h, cudaMemsetAsync(a.lz_v, 0, (size_t)P * h->n * sizeof(double), h->stream));
+  }
+  CK(h, cudaFuncSetAttribute((const void*)k_persistent<true, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->p_dyn));
+  int occ = 0;
+  CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_persistent<true, true>, PT, h->p_dyn));
+  if (occ < 1) return set_err(h, RGDBEK_E_CUDA, "Algorithm 2 kernel cannot be resident");
+  a.lzP = P;
+  a.lzGp = G / P;
+  h->pG = G;
+  h->lazyP = P;
+  CK(h, cudaStreamSynchronize(h->stream));
   return RGDBEK_OK;
 }
 

@@ -35,10 +35,12 @@ def _oracle(w):
     return Oracle(w.A, w.b, w.eta)
 
 
-def _run_parity(w, iters=50, seed=0, every=1):
+def _run_parity(w, iters=50, seed=0, every=1, lazy=0, oracle=None):
     """Step both sides one iteration at a time; compare blocks, scalars, x and z."""
     s = _solver(w)
-    o = _oracle(w)
+    if lazy:
+        s.set_lazy(lazy)
+    o = oracle if oracle is not None else _oracle(w)
     s.reset(seed)
     bn = np.linalg.norm(w.b)
     for k in range(iters):
@@ -149,6 +151,46 @@ def test_sparse_tile_edges(engine, monkeypatch):
     assert lens.max() > 512 and (lens == 512).any() and (lens == 0).any()
     assert np.bincount(w.A.indices, minlength=w.A.shape[1]).max() > 512
     _run_parity(w, 25, seed=6)
+
+
+@pytest.mark.parametrize("name,P", [("C2s", 2), ("C2s", 3), ("C2s", 4), ("C2s", 8),
+                                    ("C2si", 4), ("C1", 2)])
+def test_lazy_algorithm_2(name, P):
+    """The paper's parallel Algorithm 2 with P logical processes (rgdbek_set_lazy)
+    against oracle/lazy.py: global U, per-process J, x/z, summed scalars."""
+    from oracle.lazy import LazyOracle
+    from workloads import by_name
+    w = by_name(name)
+    _run_parity(w, 30, seed=2, lazy=P, oracle=LazyOracle(w.A, w.b, w.eta, parts=P))
+
+
+@pytest.mark.parametrize("name", ["C2s", "C2si"])
+def test_lazy_one_process_is_algorithm_1(name):
+    """set_lazy(1) runs the Algorithm 2 kernel with one process: Algorithm 1's oracle."""
+    from workloads import by_name
+    _run_parity(by_name(name), 30, seed=5, lazy=1)
+
+
+def test_lazy_argument_checks():
+    from paper_2509_19267_b200 import RgdbekError
+    from workloads import by_name
+    w = by_name("C3s")                                # sparse: not supported
+    s = _solver(w)
+    with pytest.raises(RgdbekError):
+        s.set_lazy(2)
+    s.close()
+    d = _solver(by_name("C1"))
+    with pytest.raises(RgdbekError):
+        d.set_lazy(9)
+    d.set_selection("greedy")
+    with pytest.raises(RgdbekError):
+        d.set_lazy(2)
+    d.set_selection("random")
+    d.set_lazy(2)
+    with pytest.raises(RgdbekError):
+        d.set_mode("exact")
+    d.set_lazy(0)                                     # back to Algorithm 1
+    d.close()
 
 
 def test_fat_sparse_system():
