@@ -155,15 +155,18 @@ def time_kernel(s, kernel, reps, torch):
     return e0.elapsed_time(e1) * 1e-3 / reps, bytes_per
 
 
-def cpu_oracle_sample(w, budget_s=15.0, max_iters=None, mode="pinv_free", inner=(1e-13, 200)):
+def cpu_oracle_sample(w, budget_s=15.0, max_iters=None, mode="pinv_free", inner=(1e-13, 200),
+                      lazy=0):
     """Oracle iterations/s on a bounded sample (first iterations of the same solve)."""
     from oracle import Oracle
+    from oracle.lazy import LazyOracle
     try:
         from threadpoolctl import threadpool_info
         threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
     except Exception:
         threads = os.cpu_count()
-    o = Oracle(w.A, w.b, w.eta, update=mode, inner_tol=inner[0], inner_max=inner[1])
+    o = (LazyOracle(w.A, w.b, w.eta, parts=lazy) if lazy else
+         Oracle(w.A, w.b, w.eta, update=mode, inner_tol=inner[0], inner_max=inner[1]))
     t0 = time.perf_counter()
     it = 0
     while True:
@@ -197,6 +200,8 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = by_name(args.workload)
+    if args.eta:
+        w.eta = args.eta
     m, n = w.shape
     stream = torch.cuda.current_stream()
     comm, rows = None, None
@@ -210,6 +215,8 @@ def run_ours(args):
     s = make_solver(w, local, stream.cuda_stream, rows, comm)
     if args.mode == "exact":
         s.set_mode("exact", inner_tol=args.inner_tol, inner_max=args.inner_max)
+    if args.lazy:
+        s.set_lazy(args.lazy)
     engine, ctas = s.engine_info()
     s.reset(0)
     s.step(args.warmup)                              # W untimed warm-up iterations
@@ -308,6 +315,8 @@ def run_ours(args):
                              A_host=A_h if w.dense else None, b_host=b_h)
             if args.mode == "exact":
                 s2.set_mode("exact", inner_tol=args.inner_tol, inner_max=args.inner_max)
+            if args.lazy:
+                s2.set_lazy(args.lazy)
             t1 = time.perf_counter()
             s2.reset(0)
             s2.step(args.steps)
@@ -337,6 +346,8 @@ def run_ours(args):
         os.environ["RGDBEK_PHASE_TIMING"] = "1"
         sp = make_solver(w, local, stream.cuda_stream)
         del os.environ["RGDBEK_PHASE_TIMING"]
+        if args.lazy:
+            sp.set_lazy(args.lazy)
         sp.reset(0)
         kph = min(args.steps, 300)
         sp.step(kph)
@@ -357,7 +368,8 @@ def run_ours(args):
         cpu = None
         if not args.skip_cpu:
             v, it, el, threads = cpu_oracle_sample(w, budget_s=args.cpu_budget, mode=args.mode,
-                                                   inner=(args.inner_tol, args.inner_max))
+                                                   inner=(args.inner_tol, args.inner_max),
+                                                   lazy=args.lazy)
             cpu = {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "oracle",
                    "sample": f"first {it} iterations of the same {args.workload} solve "
                              f"(seed 0) in {el:.1f} s, numpy/BLAS fp64 incl. the per-iteration RSE matvec"}
@@ -372,6 +384,8 @@ def run_ours(args):
                        "parallelism": f"rows{world} (NCCL)" if world > 1 else "single",
                        "engine": "persistent" if engine == 0 else "graph",
                        "update": args.mode,
+                       "algorithm": (f"Algorithm 2, {args.lazy} logical processes (lazy averaging)"
+                                     if args.lazy else "Algorithm 1"),
                        "l2": "inputs larger than L2 (A = %.0f MB > 126 MB)" % (
                            (m * n * 8 if w.dense else w.A.nnz * 12) / 1e6)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "time_to_tol": ttt,
@@ -443,6 +457,10 @@ def main():
     ap.add_argument("--skip-phases", action="store_true")
     ap.add_argument("--mode", default="pinv_free", choices=["pinv_free", "exact"],
                     help="exact = Alg. 1's pseudoinverse updates by inner CGLS (NEXT #1)")
+    ap.add_argument("--lazy", type=int, default=0,
+                    help="the paper's parallel Algorithm 2 with this many logical row "
+                         "processes (dense, 1 GPU); 0 = Algorithm 1")
+    ap.add_argument("--eta", type=float, default=None, help="override the workload's eta")
     ap.add_argument("--inner-tol", type=float, default=1e-13)
     ap.add_argument("--inner-max", type=int, default=200)
     args = ap.parse_args()
