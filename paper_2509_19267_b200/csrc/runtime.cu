@@ -268,14 +268,6 @@ __global__ void k_compare(const long long* a, const long long* b, long long n1, 
   }
 }
 
-__global__ void k_selmask_to_list(const unsigned char* mask, long long count, long long base,
-                                  int* out, unsigned long long* pos) {
-  // order is restored on the host (std::sort) — this is a debug/readout path only
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count;
-       i += (long long)gridDim.x * blockDim.x)
-    if (mask[i]) out[atomicAdd(pos, 1ull)] = (int)(base + i);
-}
-
 // Greedy row tiles: consecutive rows with <= TILE_NNZ nonzeros and <= TILE_ROWS rows
 // (a longer row is a tile by itself).
 rgdbek_status build_tiles(rgdbek_ctx* h, const long long* d_ptr, long long rows, int** out,
