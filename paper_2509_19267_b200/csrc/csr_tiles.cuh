@@ -24,16 +24,16 @@ namespace rg {
 
 // Geometry (compile-time; -D overrides exist for A/B builds, tools/ab_variants.py).
 #ifndef RG_TILE_NNZ
-#define RG_TILE_NNZ 512
+#define RG_TILE_NNZ 1024
 #endif
 #ifndef RG_TILE_ROWS
-#define RG_TILE_ROWS 96
+#define RG_TILE_ROWS 256
 #endif
 #ifndef RG_TBUF
 #define RG_TBUF 3
 #endif
 #ifndef RG_PEND
-#define RG_PEND 256
+#define RG_PEND 512
 #endif
 #ifndef RG_RU
 #define RG_RU 6
@@ -44,7 +44,10 @@ namespace rg {
 #ifndef RG_TILE_BLOCKED
 #define RG_TILE_BLOCKED 0
 #endif
-constexpr int TG = 128;              // threads per worker group
+#ifndef RG_TG
+#define RG_TG 256
+#endif
+constexpr int TG = RG_TG;            // threads per worker group
 constexpr int TILE_NNZ = RG_TILE_NNZ;    // nonzeros per tile
 constexpr int TILE_ROWS = RG_TILE_ROWS;  // rows per tile
 constexpr int TBUF = RG_TBUF;        // staged tiles per group (one in use, the rest in flight)

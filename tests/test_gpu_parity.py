@@ -108,33 +108,36 @@ def test_sparse_random_with_empty_rows_and_columns():
     _run_parity(w, 30, seed=2)
 
 
+TILE_NNZ, TILE_ROWS = 1024, 256        # csr_tiles.cuh defaults (RG_TILE_NNZ, RG_TILE_ROWS)
+
+
 def _tile_edge_matrix(seed=11):
-    """Row and column lengths around the sparse tile limits (csr_tiles.cuh: 512
-    nonzeros, 96 rows per tile): rows / columns longer than a tile (the group-wide
-    path, both passes), a row of exactly 512, runs of 1-nnz rows (row-limited
-    tiles), empty rows, and short rows everywhere else."""
+    """Row and column lengths around the sparse tile limits (csr_tiles.cuh:
+    TILE_NNZ nonzeros, TILE_ROWS rows per tile): rows / columns longer than a tile
+    (the group-wide path, both passes), a row of exactly TILE_NNZ, a run of 1-nnz
+    rows longer than TILE_ROWS (row-limited tiles), empty rows, short rows elsewhere."""
     import scipy.sparse as sp
     from workloads.gen import Workload
     rng = np.random.default_rng(seed)
-    m, n = 2600, 1400
+    m, n = 3000, 2400
     rows, cols = [], []
     def add_row(i, cnt):
         c = rng.choice(n, size=cnt, replace=False)
         rows.extend([i] * cnt); cols.extend(c.tolist())
     for i in range(m):
-        if i in (5, 1300, 2599):
-            add_row(i, 700)                  # longer than a tile
+        if i in (5, 1500, 2999):
+            add_row(i, TILE_NNZ + 300)        # longer than a tile
         elif i == 800:
-            add_row(i, 512)                  # exactly a tile
-        elif 1000 <= i < 1300:
-            add_row(i, 1)                    # tiles limited by rows, not nonzeros
+            add_row(i, TILE_NNZ)              # exactly a tile
+        elif 1000 <= i < 1000 + TILE_ROWS + 60:
+            add_row(i, 1)                     # tiles limited by rows, not nonzeros
         elif i % 97 == 0:
-            continue                         # empty rows
+            continue                          # empty rows
         else:
             add_row(i, int(rng.integers(2, 9)))
-    for j in (3, 777):                       # columns longer than a tile (pass T)
-        extra = rng.choice(m, size=900, replace=False)
-        rows.extend(extra.tolist()); cols.extend([j] * 900)
+    for j in (3, 777):                        # columns longer than a tile (pass T)
+        extra = rng.choice(m, size=TILE_NNZ + 500, replace=False)
+        rows.extend(extra.tolist()); cols.extend([j] * len(extra))
     A = sp.coo_matrix((rng.standard_normal(len(rows)), (rows, cols)), shape=(m, n)).tocsr()
     A.sum_duplicates(); A.sort_indices(); A.eliminate_zeros()
     b = A @ rng.standard_normal(n) + 0.05 * rng.standard_normal(m)
@@ -148,8 +151,8 @@ def test_sparse_tile_edges(engine, monkeypatch):
     monkeypatch.setenv("RGDBEK_ENGINE", engine)
     w = _tile_edge_matrix()
     lens = np.diff(w.A.indptr)
-    assert lens.max() > 512 and (lens == 512).any() and (lens == 0).any()
-    assert np.bincount(w.A.indices, minlength=w.A.shape[1]).max() > 512
+    assert lens.max() > TILE_NNZ and (lens == TILE_NNZ).any() and (lens == 0).any()
+    assert np.bincount(w.A.indices, minlength=w.A.shape[1]).max() > TILE_NNZ
     _run_parity(w, 25, seed=6)
 
 
