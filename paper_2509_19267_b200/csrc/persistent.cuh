@@ -24,7 +24,10 @@ constexpr int ZCH = 1024;                 // rows of z / xi staged per chunk (pa
 #define RG_VEC_PREFETCH 1
 #endif
 #ifndef RG_VEC_PREFETCH2
-#define RG_VEC_PREFETCH2 0
+#define RG_VEC_PREFETCH2 1      // mask sweeps (P5, P11) pipelined too: C2c +1 %, C3 +2 %, C4 -2 %
+#endif
+#ifndef RG_P11_U4
+#define RG_P11_U4 0
 #endif
 constexpr int PN_RB = 256;                // max rows per batch (dense pass N)
 constexpr int PN_QMAX = 8;                // max column chunks per row (dense pass N)
@@ -1410,19 +1413,48 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       long long cnt = 0;
       unsigned long long hs = 0ull;
 #if RG_VEC_PREFETCH2
-      const int stride = G * PT;
-      const int i0 = blockIdx.x * PT + threadIdx.x;
+      // software-pipelined: the next element's key and residual are in flight
+      const int stride = LAZY ? PT : G * PT;
+      const int i0 = LAZY ? (int)((long long)m_loc * blockIdx.x / G) + threadIdx.x
+                          : blockIdx.x * PT + threadIdx.x;
+      const int i_end = LAZY ? (int)((long long)m_loc * (blockIdx.x + 1) / G) : m_loc;
       unsigned long long nk = 0ull;
       double nr = 0.0;
-      if (i0 < m_loc) { nk = a.keys_m[i0]; nr = a.r[i0]; }
-      for (int i = i0; i < m_loc; i += stride) {
+      if (i0 < i_end) { nk = a.keys_m[i0]; nr = a.r[i0]; }
+      for (int i = i0; i < i_end; i += stride) {
         const unsigned long long ki = nk;
         const double ri = nr;
-        if (i + stride < m_loc) { nk = a.keys_m[i + stride]; nr = a.r[i + stride]; }
+        if (i + stride < i_end) { nk = a.keys_m[i + stride]; nr = a.r[i + stride]; }
         const long long gi = a.row0 + i;
         const bool sel = p_selected(&ps, ki, gi);
         a.xi[i] = sel ? ri : 0.0;
         if (sel) { Xp += ri * ri; cnt += 1; hs += splitmix64((unsigned long long)gi); }
+      }
+#elif RG_P11_U4
+      // four elements in flight per thread (8 independent loads), same per-thread order
+      const int i_beg = LAZY ? (int)((long long)m_loc * blockIdx.x / G) + threadIdx.x
+                             : blockIdx.x * PT + threadIdx.x;
+      const int i_end = LAZY ? (int)((long long)m_loc * (blockIdx.x + 1) / G) : m_loc;
+      const int step = LAZY ? PT : G * PT;
+      for (int i0 = i_beg; i0 < i_end; i0 += 4 * step) {
+        unsigned long long kv[4];
+        double rv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int i = i0 + e * step;
+          kv[e] = i < i_end ? a.keys_m[i] : KEY_NEVER;
+          rv[e] = i < i_end ? a.r[i] : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int i = i0 + e * step;
+          if (i < i_end) {
+            const long long gi = a.row0 + i;
+            const bool sel = p_selected(&ps, kv[e], gi);
+            a.xi[i] = sel ? rv[e] : 0.0;
+            if (sel) { Xp += rv[e] * rv[e]; cnt += 1; hs += splitmix64((unsigned long long)gi); }
+          }
+        }
       }
 #else
       const int i_beg = LAZY ? (int)((long long)m_loc * blockIdx.x / G) + threadIdx.x
