@@ -113,8 +113,10 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------
-def make_solver(w, device, stream, row_range=None, nccl_comm=None, A_host=None, b_host=None):
-    """The C-ABI solver for workload w (this rank's rows when row_range is given)."""
+def make_solver(w, device, stream, row_range=None, nccl_comm=None, A_host=None, b_host=None,
+                csr_host=None):
+    """The C-ABI solver for workload w (this rank's rows when row_range is given).
+    A_host / b_host / csr_host: pinned host copies (the e2e leg)."""
     from paper_2509_19267_b200 import Solver
     from paper_2509_19267_b200.dist import shard_csr
     if w.dense:
@@ -124,8 +126,8 @@ def make_solver(w, device, stream, row_range=None, nccl_comm=None, A_host=None, 
             A, b = A[row_range[0]:row_range[1]], b[row_range[0]:row_range[1]]
         return Solver(A, b, eta=w.eta, device=device, stream=stream, m=w.shape[0],
                       row_range=row_range, nccl_comm=nccl_comm)
-    rp, ci, val = w.csr_arrays()
-    b = w.b
+    rp, ci, val = w.csr_arrays() if csr_host is None else csr_host
+    b = w.b if b_host is None else b_host
     if row_range is not None:
         rp, ci, val = shard_csr(rp, ci, val, *row_range)
         b = b[row_range[0]:row_range[1]]
@@ -301,6 +303,7 @@ def run_ours(args):
     e2e = None
     if not args.skip_e2e:
         A_h = torch.from_numpy(np.ascontiguousarray(w.A)).pin_memory() if w.dense else None
+        csr_h = None if w.dense else tuple(torch.from_numpy(a).pin_memory() for a in w.csr_arrays())
         b_h = torch.from_numpy(w.b).pin_memory()
         x_h = torch.empty(n, dtype=torch.float64).pin_memory()
         # short runs are repeated (median of 3): one create() is a few ms of host work
@@ -312,7 +315,7 @@ def run_ours(args):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             s2 = make_solver(w, local, stream.cuda_stream, rows, comm,
-                             A_host=A_h if w.dense else None, b_host=b_h)
+                             A_host=A_h if w.dense else None, b_host=b_h, csr_host=csr_h)
             if args.mode == "exact":
                 s2.set_mode("exact", inner_tol=args.inner_tol, inner_max=args.inner_max)
             if args.lazy:
