@@ -29,6 +29,9 @@ constexpr int ZCH = 1024;                 // rows of z / xi staged per chunk (pa
 #ifndef RG_P11_U4
 #define RG_P11_U4 0
 #endif
+#ifndef RG_FUSE_XI
+#define RG_FUSE_XI 1      // dense: xi = r on J formed while pass T stages its rows (no P11 sweep)
+#endif
 constexpr int PN_RB = 256;                // max rows per batch (dense pass N)
 constexpr int PN_QMAX = 8;                // max column chunks per row (dense pass N)
 #ifndef RG_LOCAL_SEL_MAX
@@ -613,8 +616,14 @@ template <int KP>
 __device__ void p_dense_passT_rows(const PArgs& a, int pending, double* zs, const double* in1,
                                    const double* in2);
 
+// Optional fused row mask (psr != nullptr, RG_FUSE_XI): xi_i = r_i if row i is in
+// the row block J (psr) else 0 is formed while the rows are staged, and this
+// CTA's ||xi||^2, |J| and hash partials are returned (each row is staged by
+// exactly one CTA, counted at the first column tile only).
 __device__ void p_dense_passT(const PArgs& a, int pending, double* zs,
-                              const double* in1 = nullptr, const double* in2 = nullptr) {
+                              const double* in1 = nullptr, const double* in2 = nullptr,
+                              const PSel* psr = nullptr, double* Xp = nullptr,
+                              long long* cntp = nullptr, unsigned long long* hsp = nullptr) {
   if (!in1) in1 = a.z;
   if (!in2) in2 = a.xi;
   const int ntiles = (a.n + 2 * PT - 1) / (2 * PT);
@@ -637,7 +646,19 @@ __device__ void p_dense_passT(const PArgs& a, int pending, double* zs,
       __syncthreads();
       for (int i = threadIdx.x; i < rows; i += PT) {
         zs[i] = in1[rc + i];
-        zs[ZCH + i] = pending ? in2[rc + i] : 0.0;
+        if (psr) {
+          double xv = 0.0;
+          if (pending) {
+            const long long gi = a.row0 + rc + i;
+            if (p_selected(psr, a.keys_m[rc + i], gi)) {
+              xv = a.r[rc + i];
+              if (t == 0) { *Xp += xv * xv; *cntp += 1; *hsp += splitmix64((unsigned long long)gi); }
+            }
+          }
+          zs[ZCH + i] = xv;
+        } else {
+          zs[ZCH + i] = pending ? in2[rc + i] : 0.0;
+        }
       }
       __syncthreads();
       const double* p = a.A + (long long)rc * a.lda + c;
@@ -972,10 +993,44 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     // into the tile epilogue, so the separate P2 phase (and its barrier) vanishes.
     double Vp = 0.0, Emax = 0.0;
     if constexpr (DENSE) {
-      p_dense_passT(a, pending, dyn);
+      if constexpr (RG_FUSE_XI) {
+        // pass T forms xi_{k-1} from r and the row selection still in `ps`, and
+        // publishes ||xi||^2, |J| and hash partials (replaces the P11 sweep)
+        double Xp = 0.0;
+        long long cnt = 0;
+        unsigned long long hs = 0ull;
+        p_dense_passT(a, pending, dyn, nullptr, nullptr, &ps, &Xp, &cnt, &hs);
+        if (pending) {
+          cnt = warp_sum_ll(cnt);
+          hs = warp_sum_u64(hs);
+          if ((threadIdx.x & 31) == 0 && (cnt || hs)) {
+            atomicAdd(&a.acc[2], (unsigned long long)cnt);
+            atomicAdd(&a.acc[3], hs);
+          }
+          const double xb = pblock_sum(Xp, sh);
+          if (threadIdx.x == 0) bp[SL_X * G + blockIdx.x] = xb;
+        }
+      } else {
+        p_dense_passT(a, pending, dyn);
+      }
       grid_sync(a.bar, bgen);
       PH(1);
-      p_zero_side(a, 1);                        // m-side buffers: consumed in P9..P12
+      if constexpr (RG_FUSE_XI) {
+        // the row step k-1's |J|, hash and X (read by every CTA before the P2
+        // barrier; the m-side counters are zeroed after it, in P3)
+        if (pending) {
+          X = slot_sum(bp, SL_X, sh);
+          const long long kppf = (long long)__ldcg(&a.acc[2]);
+          const unsigned long long hashJ = __ldcg(&a.acc[3]);
+          if (lead) {
+            if (!a.greedy && !LAZY && kppf != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 2;
+            if (TraceRec* t = trace_at(tr, st, k - 1)) { t->kpp = kppf; t->hash_j = hashJ; t->X = X; }
+          }
+          kpp_prev = kppf;
+        }
+      } else {
+        p_zero_side(a, 1);                      // m-side buffers: consumed in P9..P12
+      }
       if constexpr (LAZY) {
         for (int i = blockIdx.x * PT + threadIdx.x; i < a.lzP * NBINS; i += G * PT) a.lz_hist[i] = 0u;
       }
@@ -1104,6 +1159,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     }
 
     // ===== P3: V, alpha_x; level-1 bucket (U); level-2 scan =====
+    if constexpr (DENSE && RG_FUSE_XI) p_zero_side(a, 1);   // every CTA read acc[2..3] before P2's barrier
     double V;
     if constexpr (LAZY) {
       // per-process V_p (over every CTA's columns) and X_p (the process's rows,
@@ -1407,8 +1463,8 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       // ===== P11: exact threshold =====
       p_sel_level3(&ps, hm + 2 * NBINS, cm, a.ncand + 1, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
     }
-    // ===== P11: xi = r on J, X, |J|, hash =====
-    {
+    // ===== P11: xi = r on J, X, |J|, hash (dense: fused into the next pass T) =====
+    if constexpr (!(DENSE && RG_FUSE_XI)) {
       double Xp = 0.0;
       long long cnt = 0;
       unsigned long long hs = 0ull;
@@ -1476,20 +1532,22 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       }
       const double xb = pblock_sum(Xp, sh);
       if (threadIdx.x == 0) bp[SL_X * G + blockIdx.x] = xb;
+      grid_sync(a.bar, bgen);
     }
-    grid_sync(a.bar, bgen);
     PH(10);
 
     // ===== P12: X, |J|; bookkeeping; k++ =====
-    X = slot_sum(bp, SL_X, sh);
-    const long long kpp = (long long)__ldcg(&a.acc[2]);
-    const unsigned long long hashJ = __ldcg(&a.acc[3]);
-    if (lead) {
-      if (!a.greedy && !LAZY && kpp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 2;
-      if (TraceRec* t = trace_at(tr, st, k)) { t->kpp = kpp; t->hash_j = hashJ; t->X = X; }
+    if constexpr (!(DENSE && RG_FUSE_XI)) {
+      X = slot_sum(bp, SL_X, sh);
+      const long long kpp = (long long)__ldcg(&a.acc[2]);
+      const unsigned long long hashJ = __ldcg(&a.acc[3]);
+      if (lead) {
+        if (!a.greedy && !LAZY && kpp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 2;
+        if (TraceRec* t = trace_at(tr, st, k)) { t->kpp = kpp; t->hash_j = hashJ; t->X = X; }
+      }
+      kpp_prev = kpp;
     }
     kp_prev = kp;
-    kpp_prev = kpp;
     pending = 1;
     k += 1;
     PH(0);
