@@ -220,12 +220,33 @@ __global__ void k_dense_rownorm(const double* A, long long lda, long long m, lon
   }
 }
 
-__global__ void k_dense_colnorm(const double* A, long long lda, long long m, long long n,
-                                double* out) {
+// gamma_j = sum_i A_ij^2 in two deterministic stages: blockIdx.y = a panel of
+// rows, threads = columns (coalesced), 8 rows in flight per thread; then the
+// panel partials are added in panel order.
+__global__ void k_dense_colnorm_part(const double* A, long long lda, long long m, long long n,
+                                     long long rows_per_panel, double* part) {
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const long long r0 = (long long)blockIdx.y * rows_per_panel;
+  const long long r1 = r0 + rows_per_panel < m ? r0 + rows_per_panel : m;
+  double acc = 0.0;
+  long long i = r0;
+  for (; i + 8 <= r1; i += 8) {
+    double v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = A[(i + e) * lda + j];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc = fma(v[e], v[e], acc);
+  }
+  for (; i < r1; ++i) acc = fma(A[i * lda + j], A[i * lda + j], acc);
+  part[(long long)blockIdx.y * n + j] = acc;
+}
+
+__global__ void k_dense_colnorm_sum(const double* part, long long panels, long long n, double* out) {
   for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n;
        j += (long long)gridDim.x * blockDim.x) {
     double acc = 0.0;
-    for (long long i = 0; i < m; ++i) acc = fma(A[i * lda + j], A[i * lda + j], acc);
+    for (long long p = 0; p < panels; ++p) acc += part[p * n + j];
     out[j] = acc;
   }
 }
@@ -1016,7 +1037,15 @@ rgdbek_status rgdbek_create_dense(rgdbek_handle* out, int64_t m, int64_t n, cons
   k_check_finite<<<nblocks(h->m_loc, 256, 1024), 256, 0, h->stream>>>(h->b, h->m_loc, flag);
   if ((s = check_flag(h, flag, RGDBEK_E_NONFINITE, "NaN or Inf in A or b")) != RGDBEK_OK) return create_fail(h, s);
   k_dense_rownorm<<<nblocks(h->m_loc * 32, 256, 4096), 256, 0, h->stream>>>(h->A, h->lda, h->m_loc, h->n, h->rho);
-  k_dense_colnorm<<<nblocks(h->n, 128, 4096), 128, 0, h->stream>>>(h->A, h->lda, h->m_loc, h->n, h->gamma);
+  {
+    const long long panels = std::min<long long>(64, std::max<long long>(1, h->m_loc / 64));
+    const long long rpp = (h->m_loc + panels - 1) / panels;
+    double* cpart = nullptr;
+    if ((s = dalloc(h, &cpart, (size_t)panels * h->n)) != RGDBEK_OK) return create_fail(h, s);
+    dim3 g((unsigned)((h->n + 255) / 256), (unsigned)panels);
+    k_dense_colnorm_part<<<g, 256, 0, h->stream>>>(h->A, h->lda, h->m_loc, h->n, rpp, cpart);
+    k_dense_colnorm_sum<<<nblocks(h->n, 256, 4096), 256, 0, h->stream>>>(cpart, panels, h->n, h->gamma);
+  }
   // dense pass T geometry: column tiles of 2*PT_TPB, ~8 blocks per SM in total
   h->tiles = (int)((n + 2 * PT_TPB - 1) / (2 * PT_TPB));
   int panels = std::max(1, (148 * 8 + h->tiles - 1) / h->tiles);
