@@ -24,7 +24,7 @@ namespace rg {
 
 // Geometry (compile-time; -D overrides exist for A/B builds, tools/ab_variants.py).
 #ifndef RG_TILE_NNZ
-#define RG_TILE_NNZ 1024
+#define RG_TILE_NNZ 1120
 #endif
 #ifndef RG_TILE_ROWS
 #define RG_TILE_ROWS 256
@@ -33,7 +33,7 @@ namespace rg {
 #define RG_TBUF 3
 #endif
 #ifndef RG_PEND
-#define RG_PEND 512
+#define RG_PEND 320
 #endif
 #ifndef RG_RU
 #define RG_RU 6
@@ -53,6 +53,7 @@ constexpr int TILE_ROWS = RG_TILE_ROWS;  // rows per tile
 constexpr int TBUF = RG_TBUF;        // staged tiles per group (one in use, the rest in flight)
 constexpr int TRING = 2 * TBUF;      // ring words per group: full[TBUF] mbarriers, rel[TBUF] counters
 constexpr int PEND = RG_PEND;        // pass-T columns batched for the key epilogue
+static_assert(PEND >= TILE_ROWS, "a whole tile's columns must fit the pending list");
 
 // One staged tile.  Windows are widened to 16-byte boundaries (bulk-copy
 // alignment): val from p0 & ~1, idx from p0 & ~3, rp from r0 & ~1.

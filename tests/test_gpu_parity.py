@@ -7,6 +7,9 @@ Bars (BASELINE.json north_star):
     reading R18) after every one of those iterations;
   * iterations to ||x - x*||/||x*|| <= 1e-6 within +/-2% of the oracle's.
 """
+import os
+import re
+
 import numpy as np
 import pytest
 
@@ -108,7 +111,13 @@ def test_sparse_random_with_empty_rows_and_columns():
     _run_parity(w, 30, seed=2)
 
 
-TILE_NNZ, TILE_ROWS = 1024, 256        # csr_tiles.cuh defaults (RG_TILE_NNZ, RG_TILE_ROWS)
+def _tile_default(name):                 # csr_tiles.cuh compile-time geometry
+    src = open(os.path.join(os.path.dirname(__file__), "..", "paper_2509_19267_b200", "csrc",
+                            "csr_tiles.cuh")).read()
+    return int(re.search(r"#define %s (\d+)" % name, src).group(1))
+
+
+TILE_NNZ, TILE_ROWS = _tile_default("RG_TILE_NNZ"), _tile_default("RG_TILE_ROWS")
 
 
 def _tile_edge_matrix(seed=11):
@@ -135,8 +144,8 @@ def _tile_edge_matrix(seed=11):
             continue                          # empty rows
         else:
             add_row(i, int(rng.integers(2, 9)))
-    for j in (3, 777):                        # columns longer than a tile (pass T)
-        extra = rng.choice(m, size=TILE_NNZ + 500, replace=False)
+    for j in (3, 777):                        # columns longer than a tile (pass T); row 800 stays exact
+        extra = rng.choice(np.delete(np.arange(m), 800), size=TILE_NNZ + 500, replace=False)
         rows.extend(extra.tolist()); cols.extend([j] * len(extra))
     A = sp.coo_matrix((rng.standard_normal(len(rows)), (rows, cols)), shape=(m, n)).tocsr()
     A.sum_duplicates(); A.sort_indices(); A.eliminate_zeros()
