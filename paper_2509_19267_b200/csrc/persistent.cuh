@@ -32,6 +32,9 @@ constexpr int ZCH = 1024;                 // rows of z / xi staged per chunk (pa
 #ifndef RG_SCAN_VU
 #define RG_SCAN_VU 6       // keys in flight per thread in the grid-wide level-2/3 scans (4: C3 -1.3 %)
 #endif
+#ifndef RG_PN_PIPE
+#define RG_PN_PIPE 0      // dense pass N: prefetch the next unit's first batch before reducing (parity-green; C2c -7.7 %, C1 -6.5 %: register spills at 1024 threads)
+#endif
 #ifndef RG_FUSE_XI
 #define RG_FUSE_XI 1      // dense: xi = r on J formed while pass T stages its rows (no P11 sweep)
 #endif
@@ -796,6 +799,28 @@ __device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp
     const int rows = min(per, re - r0);
     const int npairs = (rows + 1) >> 1;
     const int units = npairs * Q;                                // 2 rows x 1 chunk per unit
+#if RG_PN_PIPE
+    // the first batch of a warp's next unit is in flight while it reduces the
+    // current one (same FMA order as the plain loop: bit-identical results)
+    double2 pa[4], pb[4];
+    bool have = false;
+    if (wid < units) {
+      const int up = wid / Q, q = wid - up * Q;
+      const int rr = 2 * (RG_REV_N ? npairs - 1 - up : up);
+      const int c0 = q * CH, c1 = min(n, c0 + CH), c1e = c0 + ((c1 - c0) & ~1);
+      const double* a0 = a.A + (long long)(r0 + rr) * a.lda;
+      const double* a1 = rr + 1 < rows ? a0 + a.lda : a0;
+      const int c = c0 + lane * 2;
+      if (c + 192 < c1e) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          pa[g] = ld_stream2(a0 + c + 64 * g);
+          pb[g] = rr + 1 < rows ? ld_stream2(a1 + c + 64 * g) : make_double2(0.0, 0.0);
+        }
+        have = true;
+      }
+    }
+#endif
     for (int u = wid; u < units; u += PW) {
       const int up = u / Q, q = u - up * Q;
       const int rp = RG_REV_N ? npairs - 1 - up : up;
@@ -807,6 +832,20 @@ __device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp
       const double* a1 = two ? a0 + a.lda : a0;
       double w0 = 0.0, x0 = 0.0, w1 = 0.0, x1 = 0.0;
       int c = c0 + lane * 2;
+#if RG_PN_PIPE
+      if (have) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const double2 zc = *reinterpret_cast<const double2*>(v1s + c + 64 * g);
+          const double2 xc = *reinterpret_cast<const double2*>(v2s + c + 64 * g);
+          w0 = fma(pa[g].x, zc.x, w0); w0 = fma(pa[g].y, zc.y, w0);
+          x0 = fma(pa[g].x, xc.x, x0); x0 = fma(pa[g].y, xc.y, x0);
+          w1 = fma(pb[g].x, zc.x, w1); w1 = fma(pb[g].y, zc.y, w1);
+          x1 = fma(pb[g].x, xc.x, x1); x1 = fma(pb[g].y, xc.y, x1);
+        }
+        c += 256;
+      }
+#endif
       // batches of 4 column groups: all 8 A loads issued before any use
       for (; c + 192 < c1e; c += 256) {
         double2 va[4], vb[4];
@@ -845,6 +884,26 @@ __device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp
           x1 = fma(v1, in2[c1e], x1);
         }
       }
+#if RG_PN_PIPE
+      have = false;
+      if (u + PW < units) {
+        const int un = u + PW;
+        const int upn = un / Q, qn = un - upn * Q;
+        const int rrn = 2 * (RG_REV_N ? npairs - 1 - upn : upn);
+        const int c0n = qn * CH, c1n = min(n, c0n + CH), c1en = c0n + ((c1n - c0n) & ~1);
+        const double* a0n = a.A + (long long)(r0 + rrn) * a.lda;
+        const double* a1n = rrn + 1 < rows ? a0n + a.lda : a0n;
+        const int cn = c0n + lane * 2;
+        if (cn + 192 < c1en) {
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            pa[g] = ld_stream2(a0n + cn + 64 * g);
+            pb[g] = rrn + 1 < rows ? ld_stream2(a1n + cn + 64 * g) : make_double2(0.0, 0.0);
+          }
+          have = true;
+        }
+      }
+#endif
       w0 = warp_sum(w0); x0 = warp_sum(x0);
       w1 = warp_sum(w1); x1 = warp_sum(x1);
       if (lane == 0) {
