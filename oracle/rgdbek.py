@@ -25,14 +25,22 @@ What it computes (PAPER.md = /root/reference/PAPER.md, cited as P:<line>):
     eta^T r = ||xi||^2 = X, in place of the pseudoinverse of P:122).
   - Stop test on RSE = ||A x - b||^2 / ||b||^2 or on
     ||x - x*|| / ||x*|| (BASELINE.json metric), after each full iteration.
-* update="exact": Algorithm 1's own updates, z_{k+1} =
+* update="exact_lstsq": Algorithm 1's own updates, z_{k+1} =
   z_k - A_U A_U^+ z_k and x_{k+1} = x_k + (A^J)^+ r^J, written
   out with numpy's minimum-norm least-squares solver (lstsq) on the extracted
-  submatrices.
+  submatrices — the definition.
+* update="exact": the same projections by an inner Krylov solve from 0, CGLS in
+  place of the paper's LSQR (Remark 2), with the inner stopping rule
+  of DESIGN.md reading R1b.  Pinned to "exact_lstsq" (tests/test_oracle_exact.py);
+  the GPU exact mode is compared with both.
 * No blocking, fusion or reordering: every product is one library matvec
   (numpy BLAS for dense A, scipy.sparse for CSR A), every selection one sort.
 
-Pins (tests/test_oracle_*.py): Philox KATs; sampler inclusion probabilities
+Pins (tests/test_oracle_*.py): the norm caches rho, gamma by the paper's printed
+Frobenius norm of its FEM Poisson matrix, the rank-one closed form and
+sum rho = sum gamma = ||A||_F^2 (test_oracle_norms.py); the k = 1 selection law
+P(j) = eps_j / sum eps through column_step / row_step on systems whose scores have
+a norm-free closed form; Philox KATs; sampler inclusion probabilities
 (closed forms for k=1, k=2, exhaustive enumeration); the Pythagoras identity of
 eq:res_norm_evolve; orthogonality of both updates; reduction to
 the REK column step (P:54) and the Kaczmarz row step (P:47) at block size 1;

@@ -550,3 +550,27 @@ def test_greedy_gdbek_selection(name, update):
         assert np.linalg.norm(s.x() - o.x) <= tol * np.linalg.norm(o.x), k
         assert np.linalg.norm(s.z() - o.z) <= tol * np.linalg.norm(w.b), k
     s.close()
+
+
+@pytest.mark.parametrize("name", ["C2s", "C2si", "C3s"])
+def test_exact_mode_matches_lstsq_definition(name):
+    """NEXT #1 against the DEFINITION of Alg. 1's updates, not the CGLS
+    route: the oracle's update="exact_lstsq" (numpy minimum-norm lstsq on the extracted
+    A_U, A^J).  With converged inner solves (reading R1b) the GPU gives the same blocks
+    every iteration and x, z to 1e-8."""
+    from oracle import Oracle
+    from workloads import by_name
+    w = by_name(name)
+    s = _solver(w)
+    s.set_mode("exact", inner_tol=1e-14, inner_max=400)
+    o = Oracle(w.A, w.b, w.eta, update="exact_lstsq")
+    s.reset(3)
+    bn = np.linalg.norm(w.b)
+    for k in range(6):
+        rec = o.iterate(3)
+        s.step(1)
+        g = s.trace()[-1]
+        assert (g["kp"], g["hash_u"], g["kpp"], g["hash_j"]) == (rec.kp, rec.hash_u, rec.kpp, rec.hash_j), k
+        assert np.linalg.norm(s.x() - o.x) <= 1e-8 * np.linalg.norm(o.x), k
+        assert np.linalg.norm(s.z() - o.z) <= 1e-8 * bn, k
+    s.close()
