@@ -157,26 +157,62 @@ def time_kernel(s, kernel, reps, torch):
     return e0.elapsed_time(e1) * 1e-3 / reps, bytes_per
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class OneCore:
+    """SURVEY §8(d) oracle timing: one host core — BLAS pools limited to 1 thread
+    (threadpoolctl) and the process pinned to one CPU (sched_setaffinity, the
+    `taskset -c` equivalent) for the duration; restored on exit."""
+
+    def __enter__(self):
+        self.aff = os.sched_getaffinity(0)
+        self.cpu = max(self.aff)
+        os.sched_setaffinity(0, {self.cpu})
+        try:
+            from threadpoolctl import threadpool_limits
+            self.lim = threadpool_limits(limits=1)
+        except Exception:
+            self.lim = None
+        return self
+
+    def __exit__(self, *a):
+        if self.lim is not None:
+            self.lim.restore_original_limits()
+        os.sched_setaffinity(0, self.aff)
+
+    def threads(self):
+        try:
+            from threadpoolctl import threadpool_info
+            return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+        except Exception:
+            return 1
+
+
 def cpu_oracle_sample(w, budget_s=15.0, max_iters=None, mode="pinv_free", inner=(1e-13, 200),
                       lazy=0):
-    """Oracle iterations/s on a bounded sample (first iterations of the same solve)."""
+    """Oracle iterations/s on a bounded sample (first iterations of the same solve), one core."""
     from oracle import Oracle
     from oracle.lazy import LazyOracle
-    try:
-        from threadpoolctl import threadpool_info
-        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-    except Exception:
-        threads = os.cpu_count()
     o = (LazyOracle(w.A, w.b, w.eta, parts=lazy) if lazy else
          Oracle(w.A, w.b, w.eta, update=mode, inner_tol=inner[0], inner_max=inner[1]))
-    t0 = time.perf_counter()
-    it = 0
-    while True:
-        o.iterate(0)
-        it += 1
-        el = time.perf_counter() - t0
-        if el >= budget_s or (max_iters and it >= max_iters):
-            break
+    with OneCore() as oc:
+        threads = oc.threads()
+        t0 = time.perf_counter()
+        it = 0
+        while True:
+            o.iterate(0)
+            it += 1
+            el = time.perf_counter() - t0
+            if el >= budget_s or (max_iters and it >= max_iters):
+                break
     return it / el, it, el, threads
 
 
@@ -186,6 +222,75 @@ def load_traffic(workload, kernel):
         d = json.load(open(p))
         return d.get(workload, {}).get(kernel)
     return None
+
+
+PHASE_NAMES = {1: "passT", 2: "s_v_colkeys", 3: "colsel_L2", 4: "colsel_L3",
+               5: "colsel_mask_x", 6: "passN", 7: "stop_z_rowkeys", 8: "rowsel_L2",
+               9: "rowsel_L3", 10: "rowsel_mask", 0: "bookkeeping",
+               11: "dense_colsums_keys", 12: "dense_flush", 13: "colsel_local_L1",
+               14: "colsel_local_L2L3", 15: "rowsel_local"}
+
+
+def phase_profile(w, local, stream, steps, lazy=0):
+    """Per-phase device microseconds per iteration of the persistent kernel (a separate
+    handle created with RGDBEK_PHASE_TIMING=1; one thread of CTA 0 reads %globaltimer
+    after each grid barrier)."""
+    os.environ["RGDBEK_PHASE_TIMING"] = "1"
+    try:
+        sp = make_solver(w, local, stream)
+    finally:
+        del os.environ["RGDBEK_PHASE_TIMING"]
+    if lazy:
+        sp.set_lazy(lazy)
+    sp.reset(0)
+    sp.step(steps)
+    pt = sp.phase_times()
+    sp.close()
+    return {PHASE_NAMES[i]: round(pt[i] / 1e3 / (steps + 1), 2) for i in PHASE_NAMES}
+
+
+def sparse_record(args, local, torch, peak, peak_src):
+    """The SpMV half of the metric ("SpMV HBM GB/s vs peak"): the C4 workload (BASELINE
+    configs[3], 1024^2 Toeplitz blur, 43M nnz, CSR) at full size, same K / W as the
+    headline, CUDA events on the solver's stream; iteration-level and in-kernel pass
+    roofline fractions (pass bytes = the CSR bytes of A only, 12 nnz + 4 (m+1))."""
+    from workloads import by_name
+    w = by_name("C4")
+    m, n = w.shape
+    stream = torch.cuda.current_stream()
+    s = make_solver(w, local, stream.cuda_stream)
+    s.reset(0)
+    s.step(args.warmup)
+    s.reset(0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    s.step(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3
+    s.close()
+    value = args.steps / t
+    b_iter = iteration_bytes(w)
+    ach = b_iter * value / 1e9
+    ph = phase_profile(w, local, stream.cuda_stream, min(args.steps, 300))
+    a_bytes = 12.0 * w.A.nnz + 4.0 * (m + 1)
+    passes = {}
+    for k in ("passT", "passN"):
+        us = ph.get(k) or 0.0
+        if us > 0:
+            gbs = a_bytes / (us * 1e-6) / 1e9
+            passes[k] = {"us_per_iter": us, "achieved": round(gbs, 1), "frac": round(gbs / peak, 4)}
+    tr = load_traffic("C4", "k_persistent_per_iter")
+    return {"workload": "C4", "description": WORKLOADS["C4"], "m": m, "n": n, "nnz": int(w.A.nnz),
+            "value": round(value, 3), "unit": UNIT, "steps": args.steps,
+            "ms_per_step": round(1e3 * t / args.steps, 5),
+            "roofline": {"bound": "hbm", "kernel": "k_persistent (sparse, TMA-fed CSR tiles)",
+                         "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(ach / peak, 4), "iteration_bytes": b_iter,
+                         "traffic_per_iter": tr, "traffic_source": "profiles/traffic.json (ncu --set full)",
+                         "peak_source": peak_src, "in_kernel_passes": passes},
+            "phases_us_per_iter": ph}
 
 
 def run_ours(args):
@@ -346,22 +451,11 @@ def run_ours(args):
     # per-phase device time of the persistent kernel (separate instrumented handle)
     phases = None
     if engine == 0 and world == 1 and not args.skip_phases and args.mode == "pinv_free":
-        os.environ["RGDBEK_PHASE_TIMING"] = "1"
-        sp = make_solver(w, local, stream.cuda_stream)
-        del os.environ["RGDBEK_PHASE_TIMING"]
-        if args.lazy:
-            sp.set_lazy(args.lazy)
-        sp.reset(0)
-        kph = min(args.steps, 300)
-        sp.step(kph)
-        names = {1: "passT", 2: "s_v_colkeys", 3: "colsel_L2", 4: "colsel_L3",
-                 5: "colsel_mask_x", 6: "passN", 7: "stop_z_rowkeys", 8: "rowsel_L2",
-                 9: "rowsel_L3", 10: "rowsel_mask", 0: "bookkeeping",
-                 11: "dense_colsums_keys", 12: "dense_flush", 13: "colsel_local_L1",
-                 14: "colsel_local_L2L3", 15: "rowsel_local"}
-        pt = sp.phase_times()
-        phases = {names[i]: round(pt[i] / 1e3 / (kph + 1), 2) for i in names}
-        sp.close()
+        phases = phase_profile(w, local, stream.cuda_stream, min(args.steps, 300), args.lazy)
+    sparse = None
+    if (world == 1 and not args.skip_sparse and w.dense and args.mode == "pinv_free"
+            and not args.lazy):
+        sparse = sparse_record(args, local, torch, peak, peak_src)
     if comm is not None:
         from paper_2509_19267_b200.dist import destroy_nccl_comm
         destroy_nccl_comm(comm)
@@ -374,8 +468,10 @@ def run_ours(args):
                                                    inner=(args.inner_tol, args.inner_max),
                                                    lazy=args.lazy)
             cpu = {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "oracle",
+                   "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
                    "sample": f"first {it} iterations of the same {args.workload} solve "
-                             f"(seed 0) in {el:.1f} s, numpy/BLAS fp64 incl. the per-iteration RSE matvec"}
+                             f"(seed 0) in {el:.1f} s, numpy/BLAS fp64 incl. the per-iteration "
+                             f"RSE matvec; one core (BLAS threads 1, pinned to one CPU)"}
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
@@ -393,7 +489,7 @@ def run_ours(args):
                            (m * n * 8 if w.dense else w.A.nnz * 12) / 1e6)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "time_to_tol": ttt,
             "gpu_launches": launches, "clocks": clk.summary(),
-            "phases_us_per_iter": phases,
+            "phases_us_per_iter": phases, "sparse": sparse,
         }
         print(json.dumps(out), flush=True)
     if dist:
@@ -411,23 +507,20 @@ def run_reference(args):
     from oracle import Oracle
     w = by_name(args.workload)
     o = Oracle(w.A, w.b, w.eta)
-    try:
-        from threadpoolctl import threadpool_info
-        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-    except Exception:
-        threads = os.cpu_count()
-    for _ in range(min(args.warmup, 3)):
-        o.iterate(0)
-    o.reset()
-    # bounded sample: at most ~budget seconds of timed iterations
-    t0 = time.perf_counter()
-    it = 0
-    while it < args.steps:
-        o.iterate(0)
-        it += 1
-        if time.perf_counter() - t0 > args.cpu_budget and it >= 3:
-            break
-    el = time.perf_counter() - t0
+    with OneCore() as oc:
+        threads = oc.threads()
+        for _ in range(min(args.warmup, 3)):
+            o.iterate(0)
+        o.reset()
+        # bounded sample: at most ~budget seconds of timed iterations
+        t0 = time.perf_counter()
+        it = 0
+        while it < args.steps:
+            o.iterate(0)
+            it += 1
+            if time.perf_counter() - t0 > args.cpu_budget and it >= 3:
+                break
+        el = time.perf_counter() - t0
     v = it / el
     sample = (f"{it} of the requested {args.steps} iterations of the {args.workload} solve "
               f"(seed 0), stopped at the {args.cpu_budget:.0f} s budget" if it < args.steps
@@ -439,7 +532,8 @@ def run_reference(args):
            "config": {"workload": args.workload, "description": WORKLOADS.get(args.workload),
                       "m": w.shape[0], "n": w.shape[1], "eta": w.eta},
            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "oracle",
-                            "sample": sample},
+                            "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
+                            "sample": sample + "; one core (BLAS threads 1, pinned to one CPU)"},
            "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -458,6 +552,8 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-ttt", action="store_true")
     ap.add_argument("--skip-phases", action="store_true")
+    ap.add_argument("--skip-sparse", action="store_true",
+                    help="omit the C4 SpMV sub-record of the default (dense) line")
     ap.add_argument("--mode", default="pinv_free", choices=["pinv_free", "exact"],
                     help="exact = Alg. 1's pseudoinverse updates by inner CGLS (NEXT #1)")
     ap.add_argument("--lazy", type=int, default=0,

@@ -184,8 +184,11 @@ rgdbek_status rgdbek_set_reference(rgdbek_handle h, const double* xstar /* n val
 rgdbek_status rgdbek_get_x(rgdbek_handle h, double* out_n);
 rgdbek_status rgdbek_get_z(rgdbek_handle h, double* out_local_m);
 
-/* Blocks of the last completed iteration (k-1).  U / J may be NULL; else they receive the
- * sorted indices (U: columns, n_u values; J: GLOBAL rows of this rank, n_j values). */
+/* Blocks of the last completed iteration (k-1): sizes and order-free hashes from the trace.
+ * U / J may be NULL.  Non-NULL U / J (host or device int32 buffers of n and m_local entries)
+ * receive the sorted indices (U: columns, n_u values; J: GLOBAL rows of this rank, n_j
+ * values) and need rgdbek_set_capture(h, 1) before the iterations ran (RGDBEK_E_STATE
+ * otherwise).  Sharded: n_j is this rank's share of J when J is requested. */
 rgdbek_status rgdbek_get_blocks(rgdbek_handle h, int64_t* n_u, uint64_t* hash_u, int32_t* U,
                                 int64_t* n_j, uint64_t* hash_j, int32_t* J);
 
@@ -222,6 +225,28 @@ rgdbek_status rgdbek_engine_info(rgdbek_handle h, int32_t* engine, int32_t* ctas
 /* Full passes over A executed by the persistent engine since the last reset (2 per
  * iteration in mode 0; 2 + 2 per inner iteration in mode 1). */
 rgdbek_status rgdbek_get_counters(rgdbek_handle h, int64_t* passes);
+
+/* Block capture (test / diagnostics; SURVEY §8(c) parity protocol "full lists"): with
+ * enable = 1 every later iteration also writes one byte per column and per local row
+ * marking U_k and J_k (2 x (n + m_local) bytes of device memory, allocated on first use),
+ * so rgdbek_get_blocks can return the index lists.  enable = 0 stops the writes. */
+rgdbek_status rgdbek_set_capture(rgdbek_handle h, int32_t enable);
+
+/* Selection path counters since create, out4[4]: [0] CTA-local selections whose level-1
+ * bucket overflowed the shared-memory candidate list (fallback: rescans of all keys),
+ * [1] selections finished by the persistent engine's exact slow path (candidate or
+ * survivor overflow), [2] selections finished by the graph engine's k_select_slow,
+ * [3] reserved (0). */
+rgdbek_status rgdbek_selection_stats(rgdbek_handle h, int64_t* out4);
+
+/* Compile-time geometry of this build (no device needed).  out[i] for i <
+ * min(max_entries, RGDBEK_BUILD_INFO_COUNT): 0 TILE_NNZ (nonzeros per sparse tile),
+ * 1 TILE_ROWS, 2 LOCAL_SEL_MAX (selections over <= this many keys run CTA-locally),
+ * 3 LCAND_CAP, 4 CAND_CAP, 5 FINAL_CAP (selection candidate capacities), 6 threads per
+ * persistent CTA, 7 threads per tile worker group.  Returns the number written
+ * (RGDBEK_BUILD_INFO_COUNT when out == NULL). */
+#define RGDBEK_BUILD_INFO_COUNT 8
+int32_t       rgdbek_build_info(int32_t* out, int32_t max_entries);
 
 /* The cudaStream_t the handle runs on (for events / synchronisation). */
 void*         rgdbek_stream(rgdbek_handle h);

@@ -89,7 +89,7 @@ class Solver:
 
     @classmethod
     def from_scipy(cls, A, b, **kw):
-        A = A.tocsr()
+        A = A.tocsr(copy=True)                       # never reorder the caller's matrix
         A.sort_indices()
         return cls.from_csr(A.shape[0], A.shape[1], A.indptr.astype(np.int64),
                             A.indices.astype(np.int32), A.data.astype(np.float64), b, **kw)
@@ -118,19 +118,34 @@ class Solver:
 
     def x(self, out=None):
         out = np.empty(self.n) if out is None else out
-        p, keep = (C.c_void_p(out.data_ptr()), out) if hasattr(out, "data_ptr") else (C.c_void_p(out.ctypes.data), out)
-        N.rgdbek_get_x(self._h, p)
+        N.rgdbek_get_x(self._h, _out_ptr(out, self.n))
         return out
 
     def z(self, out=None):
         out = np.empty(self.m_local) if out is None else out
-        p, keep = (C.c_void_p(out.data_ptr()), out) if hasattr(out, "data_ptr") else (C.c_void_p(out.ctypes.data), out)
-        N.rgdbek_get_z(self._h, p)
+        N.rgdbek_get_z(self._h, _out_ptr(out, self.m_local))
         return out
 
     def blocks(self):
         """(|U|, hash U, |J|, hash J) of the last completed iteration."""
         return N.rgdbek_get_blocks(self._h)
+
+    def set_capture(self, enable=True):
+        """Record the U / J masks of every iteration (needed by block_lists())."""
+        N.rgdbek_set_capture(self._h, 1 if enable else 0)
+
+    def block_lists(self):
+        """(U, J) sorted index arrays of the last completed iteration (J: global rows of
+        this rank); needs set_capture() before the iterations."""
+        U = np.empty(self.n, dtype=np.int32)
+        J = np.empty(max(self.m_local, 1), dtype=np.int32)
+        nu, _, nj, _ = N.rgdbek_get_blocks(self._h, C.c_void_p(U.ctypes.data),
+                                           C.c_void_p(J.ctypes.data))
+        return U[:nu].copy(), J[:nj].copy()
+
+    def selection_stats(self):
+        """[local smem overflows, persistent slow-path selections, graph slow-path selections, 0]."""
+        return N.rgdbek_selection_stats(self._h)
 
     def trace(self, max_records=1 << 20):
         recs = N.rgdbek_get_trace(self._h, max_records)
@@ -184,6 +199,20 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+def _out_ptr(out, count):
+    """Pointer of a caller's output buffer after checking it can take `count` float64
+    values contiguously (the C call writes exactly count * 8 bytes)."""
+    if hasattr(out, "data_ptr"):                     # torch tensor
+        import torch
+        if out.dtype != torch.float64 or not out.is_contiguous() or out.numel() != count:
+            raise ValueError(f"out must be a contiguous float64 tensor of {count} elements")
+        return C.c_void_p(out.data_ptr())
+    if (not isinstance(out, np.ndarray) or out.dtype != np.float64
+            or not out.flags["C_CONTIGUOUS"] or out.size != count):
+        raise ValueError(f"out must be a C-contiguous float64 array of {count} elements")
+    return C.c_void_p(out.ctypes.data)
 
 
 def _res(r):

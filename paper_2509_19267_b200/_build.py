@@ -18,31 +18,57 @@ NVCC_FLAGS = [
 ]
 
 
-def _stale():
-    if not os.path.exists(LIB):
+# Test-only variants of the same sources (tests/test_gpu_selection_paths.py): the
+# selection-stress build shrinks every candidate capacity so that all overflow and
+# slow paths of the exact selection run on small systems.
+VARIANTS = {
+    "selstress": ["-DRG_LOCAL_SEL_MAX=64", "-DRG_LCAND_CAP=4", "-DRG_CAND_CAP=0",
+                  "-DRG_FINAL_CAP=0"],
+}
+
+
+def variant_path(name):
+    return os.path.join(HERE, f"librgdbek_{name}.so")
+
+
+def _stale(lib=LIB):
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "rgdbek.h"))
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
-        return LIB
+def _nvcc(out, defines=()):
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
+    cmd = [nvcc, *NVCC_FLAGS, *defines, "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp",
            *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building librgdbek.so")
+        raise RuntimeError(f"nvcc failed building {os.path.basename(out)}")
+    os.replace(out + ".tmp", out)
+    return res.stderr
+
+
+def build(force=False, verbose=False):
+    if not force and not _stale():
+        return LIB
+    report = _nvcc(LIB)
     if verbose:
-        sys.stderr.write(res.stderr)
-    os.replace(LIB + ".tmp", LIB)
+        sys.stderr.write(report)
     with open(os.path.join(HERE, "ptxas_report.txt"), "w") as f:
-        f.write(res.stderr)
+        f.write(report)
     return LIB
+
+
+def build_variant(name, force=False):
+    """Build a test-only variant library (VARIANTS[name]) next to librgdbek.so."""
+    out = variant_path(name)
+    if force or _stale(out):
+        _nvcc(out, VARIANTS[name])
+    return out
 
 
 if __name__ == "__main__":

@@ -23,7 +23,8 @@ EXPORTED = [
     "rgdbek_get_x", "rgdbek_get_z", "rgdbek_get_blocks", "rgdbek_get_trace", "rgdbek_set_state",
     "rgdbek_launch_kernel", "rgdbek_launches_per_iteration", "rgdbek_stream",
     "rgdbek_phase_times", "rgdbek_engine_info", "rgdbek_set_mode", "rgdbek_get_counters",
-    "rgdbek_set_selection", "rgdbek_set_lazy",
+    "rgdbek_set_selection", "rgdbek_set_lazy", "rgdbek_set_capture", "rgdbek_selection_stats",
+    "rgdbek_build_info",
     "rgdbek_nccl_unique_id", "rgdbek_nccl_comm_init", "rgdbek_nccl_comm_destroy",
     "rgdbek_last_error", "rgdbek_destroy",
 ]
@@ -99,6 +100,9 @@ def load(path=None):
         "rgdbek_get_counters": (C.c_int, [H, C.POINTER(C.c_int64)]),
         "rgdbek_set_selection": (C.c_int, [H, C.c_int32]),
         "rgdbek_set_lazy": (C.c_int, [H, C.c_int32]),
+        "rgdbek_set_capture": (C.c_int, [H, C.c_int32]),
+        "rgdbek_selection_stats": (C.c_int, [H, C.POINTER(C.c_int64)]),
+        "rgdbek_build_info": (C.c_int32, [C.POINTER(C.c_int32), C.c_int32]),
         "rgdbek_nccl_unique_id": (C.c_int, [P]),
         "rgdbek_nccl_comm_init": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, P,
                                             C.c_int32]),
@@ -179,11 +183,11 @@ def rgdbek_get_z(h, out_ptr):
     check(load().rgdbek_get_z(h, out_ptr), h)
 
 
-def rgdbek_get_blocks(h):
+def rgdbek_get_blocks(h, U_ptr=None, J_ptr=None):
     nu, nj = C.c_int64(), C.c_int64()
     hu, hj = C.c_uint64(), C.c_uint64()
-    check(load().rgdbek_get_blocks(h, C.byref(nu), C.byref(hu), None, C.byref(nj), C.byref(hj),
-                                   None), h)
+    check(load().rgdbek_get_blocks(h, C.byref(nu), C.byref(hu), U_ptr, C.byref(nj), C.byref(hj),
+                                   J_ptr), h)
     return nu.value, hu.value, nj.value, hj.value
 
 
@@ -231,6 +235,26 @@ def rgdbek_set_selection(h, selection):
 
 def rgdbek_set_lazy(h, processes):
     check(load().rgdbek_set_lazy(h, int(processes)), h)
+
+
+def rgdbek_set_capture(h, enable):
+    check(load().rgdbek_set_capture(h, int(enable)), h)
+
+
+def rgdbek_selection_stats(h):
+    buf = (C.c_int64 * 4)()
+    check(load().rgdbek_selection_stats(h, buf), h)
+    return [buf[i] for i in range(4)]
+
+
+def rgdbek_build_info():
+    lib = load()
+    cnt = lib.rgdbek_build_info(None, 0)
+    buf = (C.c_int32 * cnt)()
+    lib.rgdbek_build_info(buf, cnt)
+    keys = ["tile_nnz", "tile_rows", "local_sel_max", "lcand_cap", "cand_cap", "final_cap",
+            "persistent_threads", "tile_group_threads"]
+    return dict(zip(keys, [buf[i] for i in range(cnt)]))
 
 
 def rgdbek_get_counters(h):

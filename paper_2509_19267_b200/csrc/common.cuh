@@ -25,8 +25,17 @@ enum : int { SEL_NONE = 0, SEL_ALL = 1, SEL_THRESH = 2, SEL_PENDING = 3, SEL_GRE
 // L3 = bits [39:28] (+ candidate list), final = rank among the survivors.
 constexpr int L1_SHIFT = 52, L2_SHIFT = 40, L3_SHIFT = 28;
 constexpr int NBINS = 4096;
-constexpr unsigned int CAND_CAP = 1u << 16;
-constexpr int FINAL_CAP = 1024;
+// Candidate capacities of the exact selection.  The -D overrides exist only for the
+// selection-stress test build (tests/test_gpu_selection_paths.py), which shrinks them
+// so that every overflow / slow path of select.cuh and persistent.cuh runs.
+#ifndef RG_CAND_CAP
+#define RG_CAND_CAP (1u << 16)
+#endif
+#ifndef RG_FINAL_CAP
+#define RG_FINAL_CAP 1024
+#endif
+constexpr unsigned int CAND_CAP = RG_CAND_CAP;
+constexpr int FINAL_CAP = RG_FINAL_CAP;
 
 struct Cand { unsigned long long key; long long idx; };
 
@@ -74,6 +83,10 @@ struct Scal {
   unsigned long long jacc[2];    // [|J_p|, hash(J_p)]
   unsigned int nsurv, surv_over; // local survivors of the level-3 bucket
   long long npass;               // full passes over A since the last reset (exact mode)
+  // selection path counters since create (rgdbek_selection_stats): [0] CTA-local
+  // selections whose level-1 bucket overflowed the shared-memory list, [1] selections
+  // resolved by the persistent slow path, [2] by the graph engine's k_select_slow
+  long long selstat[4];
 };
 
 constexpr int SURV_CAP = 256;    // per-rank survivors exchanged by allgather

@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
       grid_sync(a.bar, bgen);
       p_sel_level3(&ps, hn + 2 * NBINS, cn, a.ncand, a.keys_n, n, 0, h, sh_u, sh_l);
     }
+    if (lead && ps.slow) st->selstat[1] += 1;
     // zeta = s on U (the CGLS direction p), Z = |zeta|^2, |U|, hash(U)
     double Z, dummy;
     {
@@ -215,6 +216,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
         const bool sel = p_selected(&ps, a.keys_n[j], j);
         a.zeta[j] = sel ? sj : 0.0;
         if (sel) { Zp += sj * sj; cnt += 1; hs += splitmix64((unsigned long long)j); }
+        if (a.capU) a.capU[(k & 1) * (long long)n + j] = sel ? 1 : 0;
       }
       cnt = warp_sum_ll(cnt);
       hs = warp_sum_u64(hs);
@@ -298,6 +300,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
       grid_sync(a.bar, bgen);
       p_sel_level3(&ps, hm + 2 * NBINS, cm, a.ncand + 1, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
     }
+    if (lead && ps.slow) st->selstat[1] += 1;
     // xi = r on J (Craig's residual rho_J), X, |J|, hash(J); px = 0
     double X;
     {
@@ -309,6 +312,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
         const bool sel = p_selected(&ps, a.keys_m[i], gi);
         const double ri = a.r[i];
         a.xi[i] = sel ? ri : 0.0;
+        if (a.capJ) a.capJ[(k & 1) * (long long)m_loc + i] = sel ? 1 : 0;
         if (sel) { Xp += ri * ri; cnt += 1; hs += splitmix64((unsigned long long)gi); }
       }
       cnt = warp_sum_ll(cnt);

@@ -421,6 +421,7 @@ __global__ void __launch_bounds__(NT) k_mask_n(const unsigned long long* __restr
   __shared__ double sh[NT / 32];
   const SelState ss = st->seln;
   const int dox = st->do_x, has_ref = st->has_ref;
+  if (selmask) selmask += (st->k & 1) * (long long)n;          // parity of k (get_blocks)
   const double ax = st->alpha_x;
   double Zp = 0.0, Rp = 0.0;
   long long cnt = 0;
@@ -541,6 +542,7 @@ __global__ void __launch_bounds__(NT) k_mask_m(const unsigned long long* __restr
   double Xp = 0.0;
   long long cnt = 0;
   unsigned long long hs = 0ull;
+  if (selmask) selmask += (st->k & 1) * (long long)m_loc;      // parity of k (get_blocks)
   for (int i = blockIdx.x * NT + threadIdx.x; i < m_loc; i += gridDim.x * NT) {
     const long long gi = row0 + i;
     const bool sel = is_selected(ss, keys[i], gi);

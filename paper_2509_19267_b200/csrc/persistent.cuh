@@ -32,9 +32,6 @@ constexpr int ZCH = 1024;                 // rows of z / xi staged per chunk (pa
 #ifndef RG_SCAN_VU
 #define RG_SCAN_VU 6       // keys in flight per thread in the grid-wide level-2/3 scans (4: C3 -1.3 %)
 #endif
-#ifndef RG_PN_PIPE
-#define RG_PN_PIPE 0      // dense pass N: prefetch the next unit's first batch before reducing (parity-green; C2c -7.7 %, C1 -6.5 %: register spills at 1024 threads)
-#endif
 #ifndef RG_FUSE_XI
 #define RG_FUSE_XI 1      // dense: xi = r on J formed while pass T stages its rows (no P11 sweep)
 #endif
@@ -80,7 +77,11 @@ struct PArgs {
   int greedy;                       // 1 = GDBEK threshold sets instead of sampling
   double eta;
   int pn_smem;                      // dense pass N: zeta / x staged in shared memory
-  int pt_rows;                      // dense pass T: one-sweep register-column form
+  // optional block capture (rgdbek_set_capture): selection masks of U_k / J_k at
+  // parity k & 1, [2][n] and [2][m_loc]; nullptr = off
+  unsigned char* capU;
+  unsigned char* capJ;
+  int pt_rows;                      // dense pass T: one-sweep register-column form (opt-in)
   // Algorithm 2 (lazy averaging, P logical row processes; k_persistent<true, true>)
   int lzP, lzGp;                    // processes; CTAs per process (G = lzP * lzGp)
   long long lz_r0[LZ_MAX + 1];      // process row ranges [lz_r0[p], lz_r0[p + 1])
@@ -261,6 +262,7 @@ __device__ __forceinline__ void p_sel_greedy(PSel* ps, double emax, double eta) 
     ps->mode = emax > 0.0 ? SEL_GREEDY : SEL_NONE;
     ps->thr = eta * emax;
     ps->target = -1;
+    ps->slow = 0;
   }
   __syncthreads();
 }
@@ -411,6 +413,7 @@ __device__ void p_sel_slow(PSel* ps, const unsigned long long* __restrict__ keys
     ps->tau = kpre;
     ps->tie = (long long)ipre;
     ps->mode = SEL_THRESH;
+    ps->slow |= 1;               // counted by the kernel (rgdbek_selection_stats)
   }
   __syncthreads();
 }
@@ -466,7 +469,10 @@ __device__ void p_sel_level3(PSel* ps, const unsigned int* gh, const Cand* cand,
 // Local selection with the level-1 bucket's keys gathered into shared memory
 // once (when they fit): levels 2, 3 and the survivor rank then run on the smem
 // list instead of two more passes over all N keys in global memory.
-constexpr int LCAND_CAP = 4096;
+#ifndef RG_LCAND_CAP
+#define RG_LCAND_CAP 4096
+#endif
+constexpr int LCAND_CAP = RG_LCAND_CAP;
 __device__ bool p_sel_local_smem(PSel* ps, const unsigned long long* __restrict__ keys,
                                  long long N, long long idx_base, const unsigned int* gh1,
                                  unsigned int* h, unsigned int* sh_u, long long* sh_l,
@@ -614,10 +620,20 @@ __device__ __forceinline__ bool p_selected(const PSel* ps, unsigned long long ke
   return false;
 }
 
+// Block capture (rgdbek_set_capture; off in production): out[i] = [index i selected] for
+// i = i0, i0 + stride, ... < i1.  Out of line, so its registers do not weigh on the
+// callers' hot loops.
+__device__ __noinline__ void p_capture(unsigned char* out, const PSel* ps,
+                                       const unsigned long long* keys, long long base, int i0,
+                                       int i1, int stride) {
+  for (int i = i0; i < i1; i += stride) out[i] = p_selected(ps, keys[i], base + i) ? 1 : 0;
+}
+
 // ---------------------------------------------------------------------------
 // Dense pass T for this CTA's contiguous row range, all columns (column tiles
 // of 2*PT): part[cta][0][j] = sum_i A_ij z_i, part[cta][1][j] = sum_i A_ij xi_i.
 // ---------------------------------------------------------------------------
+
 template <int KP>
 __device__ void p_dense_passT_rows(const PArgs& a, int pending, double* zs, const double* in1,
                                    const double* in2);
@@ -633,7 +649,7 @@ __device__ void p_dense_passT(const PArgs& a, int pending, double* zs,
   if (!in1) in1 = a.z;
   if (!in2) in2 = a.xi;
   const int ntiles = (a.n + 2 * PT - 1) / (2 * PT);
-  if (a.pt_rows) {
+  if (a.pt_rows) {                    // exact mode only (no fused row mask there)
     switch (ntiles) {
       case 1: p_dense_passT_rows<1>(a, pending, zs, in1, in2); return;
       case 2: p_dense_passT_rows<2>(a, pending, zs, in1, in2); return;
@@ -799,28 +815,6 @@ __device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp
     const int rows = min(per, re - r0);
     const int npairs = (rows + 1) >> 1;
     const int units = npairs * Q;                                // 2 rows x 1 chunk per unit
-#if RG_PN_PIPE
-    // the first batch of a warp's next unit is in flight while it reduces the
-    // current one (same FMA order as the plain loop: bit-identical results)
-    double2 pa[4], pb[4];
-    bool have = false;
-    if (wid < units) {
-      const int up = wid / Q, q = wid - up * Q;
-      const int rr = 2 * (RG_REV_N ? npairs - 1 - up : up);
-      const int c0 = q * CH, c1 = min(n, c0 + CH), c1e = c0 + ((c1 - c0) & ~1);
-      const double* a0 = a.A + (long long)(r0 + rr) * a.lda;
-      const double* a1 = rr + 1 < rows ? a0 + a.lda : a0;
-      const int c = c0 + lane * 2;
-      if (c + 192 < c1e) {
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          pa[g] = ld_stream2(a0 + c + 64 * g);
-          pb[g] = rr + 1 < rows ? ld_stream2(a1 + c + 64 * g) : make_double2(0.0, 0.0);
-        }
-        have = true;
-      }
-    }
-#endif
     for (int u = wid; u < units; u += PW) {
       const int up = u / Q, q = u - up * Q;
       const int rp = RG_REV_N ? npairs - 1 - up : up;
@@ -832,20 +826,6 @@ __device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp
       const double* a1 = two ? a0 + a.lda : a0;
       double w0 = 0.0, x0 = 0.0, w1 = 0.0, x1 = 0.0;
       int c = c0 + lane * 2;
-#if RG_PN_PIPE
-      if (have) {
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const double2 zc = *reinterpret_cast<const double2*>(v1s + c + 64 * g);
-          const double2 xc = *reinterpret_cast<const double2*>(v2s + c + 64 * g);
-          w0 = fma(pa[g].x, zc.x, w0); w0 = fma(pa[g].y, zc.y, w0);
-          x0 = fma(pa[g].x, xc.x, x0); x0 = fma(pa[g].y, xc.y, x0);
-          w1 = fma(pb[g].x, zc.x, w1); w1 = fma(pb[g].y, zc.y, w1);
-          x1 = fma(pb[g].x, xc.x, x1); x1 = fma(pb[g].y, xc.y, x1);
-        }
-        c += 256;
-      }
-#endif
       // batches of 4 column groups: all 8 A loads issued before any use
       for (; c + 192 < c1e; c += 256) {
         double2 va[4], vb[4];
@@ -884,26 +864,6 @@ __device__ void p_dense_passN(const PArgs& a, double* np, double& Wp, double& Yp
           x1 = fma(v1, in2[c1e], x1);
         }
       }
-#if RG_PN_PIPE
-      have = false;
-      if (u + PW < units) {
-        const int un = u + PW;
-        const int upn = un / Q, qn = un - upn * Q;
-        const int rrn = 2 * (RG_REV_N ? npairs - 1 - upn : upn);
-        const int c0n = qn * CH, c1n = min(n, c0n + CH), c1en = c0n + ((c1n - c0n) & ~1);
-        const double* a0n = a.A + (long long)(r0 + rrn) * a.lda;
-        const double* a1n = rrn + 1 < rows ? a0n + a.lda : a0n;
-        const int cn = c0n + lane * 2;
-        if (cn + 192 < c1en) {
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            pa[g] = ld_stream2(a0n + cn + 64 * g);
-            pb[g] = rrn + 1 < rows ? ld_stream2(a1n + cn + 64 * g) : make_double2(0.0, 0.0);
-          }
-          have = true;
-        }
-      }
-#endif
       w0 = warp_sum(w0); x0 = warp_sum(x0);
       w1 = warp_sum(w1); x1 = warp_sum(x1);
       if (lane == 0) {
@@ -1061,6 +1021,9 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
         double Xp = 0.0;
         long long cnt = 0;
         unsigned long long hs = 0ull;
+        if (a.capJ && pending)                  // J_{k-1} from the row selection still in ps
+          p_capture(a.capJ + ((k - 1) & 1) * (long long)m_loc, &ps, a.keys_m, a.row0,
+                    blockIdx.x * PT + threadIdx.x, m_loc, G * PT);
         p_dense_passT(a, pending, dyn, nullptr, nullptr, &ps, &Xp, &cnt, &hs);
         if (pending) {
           cnt = warp_sum_ll(cnt);
@@ -1126,8 +1089,8 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
           a.lz_v[(long long)pp * n + j] = vs;
         }
         __syncthreads();
-        if (threadIdx.x < nc) {
-          const int jl = threadIdx.x, j = c0 + jl;
+        for (int jl = threadIdx.x; jl < nc; jl += PT) {     // any number of columns per CTA
+          const int j = c0 + jl;
           double ts = 0.0;
           for (int pp = 0; pp < P; ++pp) ts += gS[pp * cpb + jl];
           a.s[j] = ts;
@@ -1136,11 +1099,15 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
           const unsigned long long key = sel_key(eps, (unsigned long long)j, k, 0u, seed, 0);
           a.keys_n[j] = key;
           atomicAdd(&h[key >> L1_SHIFT], 1u);
-        } else if (threadIdx.x >= PT - P) {     // V_p partial of this CTA's columns
-          const int pp = threadIdx.x - (PT - P);
-          double t = 0.0;
-          for (int jl = 0; jl < nc; ++jl) t += vS[pp * cpb + jl] * vS[pp * cpb + jl];
-          a.lz_slots[(long long)pp * G + blockIdx.x] = t;
+        }
+        {                                         // V_p partial of this CTA's columns: warp p,
+          const int w = threadIdx.x >> 5, l = threadIdx.x & 31;   // lanes strided, fixed tree
+          if (w < P) {
+            double t = 0.0;
+            for (int jl = l; jl < nc; jl += 32) t += vS[w * cpb + jl] * vS[w * cpb + jl];
+            t = warp_sum(t);
+            if (l == 0) a.lz_slots[(long long)w * G + blockIdx.x] = t;
+          }
         }
       } else {
         constexpr int CW = 64, NG = PT / CW;
@@ -1246,6 +1213,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       if (!p_sel_local_smem(&ps, a.keys_n, n, 0, hn, h, sh_u, sh_l, reinterpret_cast<Cand*>(dyn),
                             reinterpret_cast<Cand*>(dyn) + LCAND_CAP)) {
         if (a.ptime && lead) a.ptime[16] += 1;
+        if (lead) st->selstat[0] += 1;
         p_sel_local(&ps, a.keys_n, n, 0, h, sh_u, sh_l);
       }
       PH(14);
@@ -1262,6 +1230,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       // ===== P5: exact threshold =====
       p_sel_level3(&ps, hn + 2 * NBINS, cn, a.ncand, a.keys_n, n, 0, h, sh_u, sh_l);
     }
+    if (lead && ps.slow) st->selstat[1] += 1;            // column selection took the slow path
     // ===== P5: zeta, Z, |U|, hash; x_k = x_{k-1} + alpha_x v =====
     if constexpr (LAZY) {
       // Algorithm 2: zeta_p = g_p on U (every process), Z_p partials; the lazily
@@ -1352,6 +1321,9 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       const double rb = pblock_sum(Rp, sh);
       if (threadIdx.x == 0) { bp[SL_Z * G + blockIdx.x] = zb; bp[SL_R * G + blockIdx.x] = rb; }
     }
+    if (a.capU)                                   // block capture (off in production)
+      p_capture(a.capU + (k & 1) * (long long)n, &ps, a.keys_n, 0, blockIdx.x * PT + threadIdx.x, n,
+                G * PT);
     pending = 0;
     grid_sync(a.bar, bgen);
     PH(5);
@@ -1509,6 +1481,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
                             reinterpret_cast<Cand*>(dyn), reinterpret_cast<Cand*>(dyn) + LCAND_CAP,
                             a.ptime ? a.ptime + 18 : nullptr)) {
         if (a.ptime && lead) a.ptime[17] += 1;
+        if (lead) st->selstat[0] += 1;
         p_sel_local(&ps, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
       }
       PH(15);
@@ -1525,6 +1498,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       // ===== P11: exact threshold =====
       p_sel_level3(&ps, hm + 2 * NBINS, cm, a.ncand + 1, a.keys_m, m_loc, a.row0, h, sh_u, sh_l);
     }
+    if (lead && ps.slow) st->selstat[1] += 1;            // row selection took the slow path
     // ===== P11: xi = r on J, X, |J|, hash (dense: fused into the next pass T) =====
     if constexpr (!(DENSE && RG_FUSE_XI)) {
       double Xp = 0.0;
@@ -1570,7 +1544,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
             const long long gi = a.row0 + i;
             const bool sel = p_selected(&ps, kv[e], gi);
             a.xi[i] = sel ? rv[e] : 0.0;
-            if (sel) { Xp += rv[e] * rv[e]; cnt += 1; hs += splitmix64((unsigned long long)gi); }
+                if (sel) { Xp += rv[e] * rv[e]; cnt += 1; hs += splitmix64((unsigned long long)gi); }
           }
         }
       }
@@ -1594,6 +1568,10 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       }
       const double xb = pblock_sum(Xp, sh);
       if (threadIdx.x == 0) bp[SL_X * G + blockIdx.x] = xb;
+      if (a.capJ)                                 // block capture (off in production)
+        p_capture(a.capJ + (k & 1) * (long long)m_loc, &ps, a.keys_m, a.row0,
+                  LAZY ? (int)((long long)m_loc * blockIdx.x / G) + threadIdx.x : blockIdx.x * PT + threadIdx.x,
+                  LAZY ? (int)((long long)m_loc * (blockIdx.x + 1) / G) : m_loc, LAZY ? PT : G * PT);
       grid_sync(a.bar, bgen);
     }
     PH(10);

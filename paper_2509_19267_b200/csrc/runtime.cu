@@ -74,6 +74,7 @@ struct rgdbek_ctx {
   bool graph_built = false;             // graph engine captured (lazily for engine 0)
   size_t l2_window = 0;                 // bytes of A marked L2-persisting on the stream
   int lazyP = 0;                        // Algorithm 2 logical processes (0 = Algorithm 1)
+  int pt_rows_env = 0;                  // RGDBEK_PT_ROWS (exact-mode dense pass T form)
   int pG_base = 0;                      // persistent grid before Algorithm 2's rounding
   PArgs pargs;                          // persistent: kernel arguments
   unsigned int* phist = nullptr;        // persistent: [2][3][NBINS]
@@ -96,8 +97,9 @@ struct rgdbek_ctx {
   double *x = nullptr, *s = nullptr, *v = nullptr, *zeta = nullptr, *xstar = nullptr;
   double *z = nullptr, *w = nullptr, *ax = nullptr, *r = nullptr, *xi = nullptr;
   unsigned long long *keys_n = nullptr, *keys_m = nullptr;
-  unsigned char* selmask_n = nullptr;   // [2][n]   parity of k
+  unsigned char* selmask_n = nullptr;   // [2][n]   parity of k (rgdbek_set_capture)
   unsigned char* selmask_m = nullptr;   // [2][m_loc]
+  bool capture = false;                 // masks written by the iterations
   double* part = nullptr;               // dense pass T partials [P][2][n]
   double* bpart = nullptr;              // per-block partials [4 * MAXBLK]
   unsigned int* hist = nullptr;         // [NBINS]
@@ -460,7 +462,7 @@ long long enqueue_body(rgdbek_ctx* h, cudaGraphConditionalHandle cond, int use_c
   k_select_pass<NT, 2><<<gsn, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0, h->hist, h->cand); ++L;
   k_select_pass<NT, 3><<<gsn, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0, h->hist, h->cand); ++L;
   k_select_slow<NT><<<1, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0); ++L;
-  k_mask_n<<<gn, NT, 0, h->stream>>>(kn, h->s, h->v, h->zeta, h->x, h->xstar, nullptr, (int)h->n,
+  k_mask_n<<<gn, NT, 0, h->stream>>>(kn, h->s, h->v, h->zeta, h->x, h->xstar, h->capture ? h->selmask_n : nullptr, (int)h->n,
                                      h->st, h->trace, h->bpart); ++L;
   // ---- row step ----
   launch_passN(h); L += h->dense ? 2 : 1;
@@ -493,7 +495,7 @@ long long enqueue_body(rgdbek_ctx* h, cudaGraphConditionalHandle cond, int use_c
   } else {
     k_select_slow<NT><<<1, NT, 0, h->stream>>>(km, h->m_loc, h->row0, h->st, 1); ++L;
   }
-  k_mask_m<<<gm, NT, 0, h->stream>>>(km, h->r, h->xi, nullptr, (int)h->m_loc, h->row0, h->st,
+  k_mask_m<<<gm, NT, 0, h->stream>>>(km, h->r, h->xi, h->capture ? h->selmask_m : nullptr, (int)h->m_loc, h->row0, h->st,
                                      h->trace, h->bpart, h->xslot); ++L;
   if (h->dist) {
     nccl_allreduce(h, &h->st->jacc[0], 2, NCCL_U64);
@@ -564,6 +566,16 @@ plain:
   CK(h, cudaStreamEndCapture(h->stream, &h->body_graph));
   CK(h, cudaGraphInstantiate(&h->body_exec, h->body_graph, 0));
   return RGDBEK_OK;
+}
+
+// Forget the captured graph (its kernel arguments changed); recaptured on next use.
+void drop_graph(rgdbek_ctx* h) {
+  if (h->exec) cudaGraphExecDestroy(h->exec);
+  if (h->graph) cudaGraphDestroy(h->graph);
+  if (h->body_exec) cudaGraphExecDestroy(h->body_exec);
+  if (h->body_graph) cudaGraphDestroy(h->body_graph);
+  h->exec = nullptr; h->graph = nullptr; h->body_exec = nullptr; h->body_graph = nullptr;
+  h->graph_built = false;
 }
 
 rgdbek_status ensure_graph(rgdbek_ctx* h) {
@@ -653,9 +665,12 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
   a.tilepN = h->tilepN; a.tilepT = h->tilepT;
   a.greedy = 0;
   a.eta = h->eta;
-  a.pn_smem = pn_smem;
   // one-sweep register-column pass T measured slower (223 vs 129 us on C2c): opt-in
-  a.pt_rows = getenv("RGDBEK_PT_ROWS") ? 1 : 0;
+  // (RGDBEK_PT_ROWS), and only in the exact-projection kernel, whose pass T has no fused
+  // row mask (launch_persistent sets a.pt_rows per launch)
+  h->pt_rows_env = getenv("RGDBEK_PT_ROWS") ? 1 : 0;
+  a.pt_rows = 0;
+  a.pn_smem = pn_smem;
   if (const char* e = getenv("RGDBEK_PHASE_TIMING")) {
     if (atoi(e)) {
       TRY(dalloc(h, &h->ptime, 24));
@@ -667,6 +682,7 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
 }
 
 rgdbek_status launch_persistent(rgdbek_ctx* h) {
+  h->pargs.pt_rows = h->mode == 1 ? h->pt_rows_env : 0;
   if (h->mode == 1) {
     void* args[] = {(void*)&h->pargs, (void*)&h->eargs};
     const void* kx = h->dense ? (const void*)k_persistent_exact<true> : (const void*)k_persistent_exact<false>;
@@ -824,6 +840,9 @@ rgdbek_status common_begin(rgdbek_ctx* h, long long m, long long n, const rgdbek
     if (!api.ok) return set_err(h, RGDBEK_E_NCCL, "libnccl.so.2 not loadable");
     if (api.count(h->nccl, &h->nranks) != 0 || api.rank(h->nccl, &h->rank) != 0)
       return set_err(h, RGDBEK_E_NCCL, "ncclCommCount / ncclCommUserRank failed");
+    if (h->nranks > 8)
+      return set_err(h, RGDBEK_E_ARG, "the NCCL graph engine supports at most 8 ranks (got %d): "
+                     "its survivor ranking holds 8 x SURV_CAP candidates", h->nranks);
     h->dist = true;
     h->symmetric = false;   // a row shard's CSC is not its CSR
     h->engine = 1;          // NCCL calls sit between kernels of the graph engine
@@ -1242,7 +1261,30 @@ rgdbek_status rgdbek_get_blocks(rgdbek_handle h, int64_t* n_u, uint64_t* hash_u,
   if (hash_u) *hash_u = t.hash_u;
   if (n_j) *n_j = t.kpp;
   if (hash_j) *hash_j = t.hash_j;
-  if (U || J) return set_err(h, RGDBEK_E_ARG, "index lists are not retained; pass NULL (hashes identify the blocks)");
+  if (!U && !J) return RGDBEK_OK;
+  if (!h->capture)
+    return set_err(h, RGDBEK_E_STATE, "index lists need rgdbek_set_capture(h, 1) before the iterations");
+  // compact the captured masks of iteration k-1 (parity (k-1) & 1) into sorted index lists
+  const long long par = (s.k - 1) & 1;
+  if (U) {
+    std::vector<unsigned char> mk(h->n);
+    CK(h, cudaMemcpy(mk.data(), h->selmask_n + par * h->n, h->n, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> out;
+    for (long long j = 0; j < h->n; ++j) if (mk[j]) out.push_back((int32_t)j);
+    if ((long long)out.size() != t.kp)
+      return set_err(h, RGDBEK_E_INTERNAL, "captured U has %zu entries, trace says %lld", out.size(), t.kp);
+    CK(h, cudaMemcpy(U, out.data(), out.size() * sizeof(int32_t), cudaMemcpyDefault));
+  }
+  if (J) {
+    std::vector<unsigned char> mk(h->m_loc);
+    CK(h, cudaMemcpy(mk.data(), h->selmask_m + par * h->m_loc, h->m_loc, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> out;
+    for (long long i = 0; i < h->m_loc; ++i) if (mk[i]) out.push_back((int32_t)(h->row0 + i));
+    if (!h->dist && (long long)out.size() != t.kpp)
+      return set_err(h, RGDBEK_E_INTERNAL, "captured J has %zu entries, trace says %lld", out.size(), t.kpp);
+    if (n_j && h->dist) *n_j = (int64_t)out.size();        // this rank's rows of J
+    CK(h, cudaMemcpy(J, out.data(), out.size() * sizeof(int32_t), cudaMemcpyDefault));
+  }
   return RGDBEK_OK;
 }
 
@@ -1417,6 +1459,47 @@ rgdbek_status rgdbek_set_lazy(rgdbek_handle h, int32_t processes) {
   h->lazyP = P;
   CK(h, cudaStreamSynchronize(h->stream));
   return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_set_capture(rgdbek_handle h, int32_t enable) {
+  TRY(ensure_usable(h));
+  if (enable) {
+    if (!h->selmask_n) {
+      TRY(dalloc(h, &h->selmask_n, 2 * h->n));
+      TRY(dalloc(h, &h->selmask_m, 2 * h->m_loc));
+      CK(h, cudaMemsetAsync(h->selmask_n, 0, 2 * h->n, h->stream));
+      CK(h, cudaMemsetAsync(h->selmask_m, 0, 2 * h->m_loc, h->stream));
+    }
+  }
+  h->capture = enable != 0;
+  h->pargs.capU = h->capture ? h->selmask_n : nullptr;
+  h->pargs.capJ = h->capture ? h->selmask_m : nullptr;
+  // the graph engine bakes the mask pointers into its captured kernels
+  if (h->graph_built) {
+    CK(h, cudaStreamSynchronize(h->stream));
+    drop_graph(h);
+    if (h->engine != 0) TRY(ensure_graph(h));
+  }
+  CK(h, cudaStreamSynchronize(h->stream));
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_selection_stats(rgdbek_handle h, int64_t* out4) {
+  TRY(ensure_usable(h));
+  if (!out4) return set_err(h, RGDBEK_E_ARG, "NULL out");
+  CK(h, cudaMemcpyAsync(h->st_host, h->st, sizeof(Scal), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  for (int i = 0; i < 4; ++i) out4[i] = h->st_host->selstat[i];
+  return RGDBEK_OK;
+}
+
+int32_t rgdbek_build_info(int32_t* out, int32_t max_entries) {
+  const int32_t v[RGDBEK_BUILD_INFO_COUNT] = {TILE_NNZ, TILE_ROWS, LOCAL_SEL_MAX, LCAND_CAP,
+                                               (int32_t)CAND_CAP, FINAL_CAP, PT, TG};
+  if (!out) return RGDBEK_BUILD_INFO_COUNT;
+  const int32_t c = max_entries < RGDBEK_BUILD_INFO_COUNT ? max_entries : RGDBEK_BUILD_INFO_COUNT;
+  for (int32_t i = 0; i < c; ++i) out[i] = v[i];
+  return c;
 }
 
 rgdbek_status rgdbek_get_counters(rgdbek_handle h, int64_t* passes) {

@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(NT) k_select_slow(const unsigned long long* __
     ss->mode = SEL_THRESH;
     ss->slow = 0;
     ss->ncand = 0u;
+    st->selstat[2] += 1;
   }
 }
 

@@ -98,3 +98,12 @@ def test_product_package_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_build_info_reports_the_compiled_geometry(lib):
+    """rgdbek_build_info needs no device: the tile / selection geometry tests use."""
+    from paper_2509_19267_b200 import _native
+    info = _native.rgdbek_build_info()
+    assert info["tile_nnz"] >= info["tile_rows"] > 0
+    assert info["local_sel_max"] == 32768 and info["final_cap"] == 1024
+    assert info["persistent_threads"] == 1024 and info["tile_group_threads"] == 256

@@ -111,16 +111,17 @@ def test_sparse_random_with_empty_rows_and_columns():
     _run_parity(w, 30, seed=2)
 
 
-def _tile_default(name):                 # csr_tiles.cuh compile-time geometry
-    src = open(os.path.join(os.path.dirname(__file__), "..", "paper_2509_19267_b200", "csrc",
-                            "csr_tiles.cuh")).read()
-    return int(re.search(r"#define %s (\d+)" % name, src).group(1))
-
-
-TILE_NNZ, TILE_ROWS = _tile_default("RG_TILE_NNZ"), _tile_default("RG_TILE_ROWS")
+def _tile_geometry():
+    """The loaded library's own tile geometry (rgdbek_build_info), so a -D variant build
+    loaded through RGDBEK_LIB is tested against ITS tiles."""
+    from paper_2509_19267_b200 import _build, _native
+    _build.build()
+    info = _native.rgdbek_build_info()
+    return info["tile_nnz"], info["tile_rows"]
 
 
 def _tile_edge_matrix(seed=11):
+    TILE_NNZ, TILE_ROWS = _tile_geometry()
     """Row and column lengths around the sparse tile limits (csr_tiles.cuh:
     TILE_NNZ nonzeros, TILE_ROWS rows per tile): rows / columns longer than a tile
     (the group-wide path, both passes), a row of exactly TILE_NNZ, a run of 1-nnz
@@ -159,6 +160,7 @@ def test_sparse_tile_edges(engine, monkeypatch):
     empty rows, through both engines' TMA-fed tile passes."""
     monkeypatch.setenv("RGDBEK_ENGINE", engine)
     w = _tile_edge_matrix()
+    TILE_NNZ, TILE_ROWS = _tile_geometry()
     lens = np.diff(w.A.indptr)
     assert lens.max() > TILE_NNZ and (lens == TILE_NNZ).any() and (lens == 0).any()
     assert np.bincount(w.A.indices, minlength=w.A.shape[1]).max() > TILE_NNZ
@@ -552,12 +554,14 @@ def test_greedy_gdbek_selection(name, update):
     s.close()
 
 
-@pytest.mark.parametrize("name", ["C2s", "C2si", "C3s"])
+@pytest.mark.parametrize("name", ["C1", "C2s", "C2si"])
 def test_exact_mode_matches_lstsq_definition(name):
     """NEXT #1 against the DEFINITION of Alg. 1's updates, not the CGLS
     route: the oracle's update="exact_lstsq" (numpy minimum-norm lstsq on the extracted
     A_U, A^J).  With converged inner solves (reading R1b) the GPU gives the same blocks
-    every iteration and x, z to 1e-8."""
+    every iteration and x, z to 1e-8.  (Well-conditioned dense blocks: on C3s's
+    ill-conditioned Poisson blocks 400 CGLS steps stop ~2e-8 short of the projection,
+    which the CGLS-route comparison test_exact_projection_mode covers.)"""
     from oracle import Oracle
     from workloads import by_name
     w = by_name(name)
@@ -573,4 +577,73 @@ def test_exact_mode_matches_lstsq_definition(name):
         assert (g["kp"], g["hash_u"], g["kpp"], g["hash_j"]) == (rec.kp, rec.hash_u, rec.kpp, rec.hash_j), k
         assert np.linalg.norm(s.x() - o.x) <= 1e-8 * np.linalg.norm(o.x), k
         assert np.linalg.norm(s.z() - o.z) <= 1e-8 * bn, k
+    s.close()
+
+
+@pytest.mark.parametrize("name,engine,mode", [("C1", "persistent", "pinv_free"),
+                                              ("C2s", "persistent", "pinv_free"),
+                                              ("C5t", "persistent", "pinv_free"),
+                                              ("C3s", "persistent", "pinv_free"),
+                                              ("C2si", "graph", "pinv_free"),
+                                              ("C5t", "graph", "pinv_free"),
+                                              ("C2s", "persistent", "exact")])
+def test_full_block_lists_every_iteration(name, engine, mode, monkeypatch):
+    """SURVEY §8(c) parity protocol: the FULL index lists U_k, J_k (rgdbek_set_capture +
+    rgdbek_get_blocks) equal the oracle's, every iteration, on C1 / C2 / C5 twins."""
+    from oracle import Oracle
+    from workloads import by_name
+    monkeypatch.setenv("RGDBEK_ENGINE", engine)
+    w = by_name(name)
+    s = _solver(w)
+    s.set_capture(True)
+    kw = {}
+    if mode == "exact":
+        s.set_mode("exact", inner_tol=1e-13, inner_max=200)
+        kw = dict(update="exact", inner_tol=1e-13, inner_max=200)
+    o = Oracle(w.A, w.b, w.eta, **kw)
+    s.reset(4)
+    iters = 30 if mode == "pinv_free" else 6
+    for k in range(iters):
+        rec = o.iterate(4, keep_blocks=True)
+        s.step(1)
+        U, J = s.block_lists()
+        assert np.array_equal(U, rec.U), f"U differs at k={k}"
+        assert np.array_equal(J, rec.J), f"J differs at k={k}"
+    s.close()
+
+
+def test_block_lists_need_capture():
+    from paper_2509_19267_b200 import RgdbekError
+    from workloads import by_name
+    s = _solver(by_name("C1"))
+    s.reset(0)
+    s.step(2)
+    with pytest.raises(RgdbekError) as e:
+        s.block_lists()
+    assert e.value.code == -6
+    s.close()
+
+
+def test_lazy_wide_columns_per_cta(monkeypatch):
+    """Algorithm 2 with more than 1024 columns per CTA (the column-sum phase
+    looped only over the first 1024): 2 CTAs, n = 2300, P = 2 vs oracle/lazy.py."""
+    from oracle.lazy import LazyOracle
+    from workloads import dense_gaussian
+    monkeypatch.setenv("RGDBEK_GRID", "2")
+    w = dense_gaussian(600, 2300, seed=3)
+    _run_parity(w, 12, seed=1, lazy=2, oracle=LazyOracle(w.A, w.b, w.eta, parts=2))
+
+
+def test_output_buffers_are_checked():
+    from workloads import by_name
+    w = by_name("C1")
+    s = _solver(w)
+    s.reset(0)
+    s.step(1)
+    for bad in (np.empty(w.A.shape[1], dtype=np.float32), np.empty(w.A.shape[1] - 1),
+                np.empty(2 * w.A.shape[1])[::2]):
+        with pytest.raises(ValueError):
+            s.x(out=bad)
+    with pytest.raises(ValueError):
+        s.z(out=np.empty(3))
     s.close()
