@@ -312,14 +312,21 @@ def run_ours(args):
     m, n = w.shape
     stream = torch.cuda.current_stream()
     comm, rows = None, None
+    use_nccl = args.multi == "nccl"
     if world > 1:
-        # row-sharded solve of ONE system (strong scaling): nnz-balanced row blocks
-        # (P:443), [A_p^T z_p | A_p^T xi_p | X_p] and a few small allreduces per iteration
+        # row-sharded solve of ONE system (strong scaling): nnz-balanced row blocks.
+        # Default: the peer-memory sharded engine (one persistent kernel per GPU, window
+        # partials / halos / histograms over NVLink, sharded.cuh); --multi nccl: the NCCL
+        # graph engine ([A_p^T z_p | A_p^T xi_p | X_p] allreduce and small collectives)
         from paper_2509_19267_b200.dist import init_nccl_comm, partition_rows
         parts = partition_rows(m if w.dense else w.A.indptr, world)
         rows = parts[rank]
-        comm = init_nccl_comm(local)
+        if use_nccl:
+            comm = init_nccl_comm(local)
     s = make_solver(w, local, stream.cuda_stream, rows, comm)
+    if world > 1 and not use_nccl:
+        from paper_2509_19267_b200.dist import connect_peers
+        connect_peers(s)
     if args.mode == "exact":
         s.set_mode("exact", inner_tol=args.inner_tol, inner_max=args.inner_max)
     if args.lazy:
@@ -421,6 +428,9 @@ def run_ours(args):
             t0 = time.perf_counter()
             s2 = make_solver(w, local, stream.cuda_stream, rows, comm,
                              A_host=A_h if w.dense else None, b_host=b_h, csr_host=csr_h)
+            if world > 1 and not use_nccl:
+                from paper_2509_19267_b200.dist import connect_peers
+                connect_peers(s2)
             if args.mode == "exact":
                 s2.set_mode("exact", inner_tol=args.inner_tol, inner_max=args.inner_max)
             if args.lazy:
@@ -480,7 +490,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.workload, "description": WORKLOADS.get(args.workload),
                        "m": m, "n": n, "nnz": int(w.nnz), "eta": w.eta,
-                       "parallelism": f"rows{world} (NCCL)" if world > 1 else "single",
+                       "parallelism": (f"rows{world} ({'NCCL graph engine' if use_nccl else 'peer-memory sharded persistent kernel'})"
+                                       if world > 1 else "single"),
                        "engine": "persistent" if engine == 0 else "graph",
                        "update": args.mode,
                        "algorithm": (f"Algorithm 2, {args.lazy} logical processes (lazy averaging)"
@@ -560,6 +571,8 @@ def main():
                     help="the paper's parallel Algorithm 2 with this many logical row "
                          "processes (dense, 1 GPU); 0 = Algorithm 1")
     ap.add_argument("--eta", type=float, default=None, help="override the workload's eta")
+    ap.add_argument("--multi", default="peer", choices=["peer", "nccl"],
+                    help="multi-GPU engine: peer-memory sharded kernel (default) or NCCL graph engine")
     ap.add_argument("--inner-tol", type=float, default=1e-13)
     ap.add_argument("--inner-max", type=int, default=200)
     args = ap.parse_args()

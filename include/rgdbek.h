@@ -38,9 +38,10 @@
  *    synchronise that stream before returning.
  *  - Multi-GPU: each rank creates its handle with the GLOBAL m, n, its own
  *    contiguous global row range [row_begin, row_end) and its local rows of A
- *    and b (column indices global), plus an ncclComm_t in options.nccl_comm.
- *    x (n) is replicated; z (local rows) is sharded.  Results are identical
- *    on every rank.
+ *    and b (column indices global), plus either an ncclComm_t in
+ *    options.nccl_comm (the NCCL graph engine: x replicated) or no communicator
+ *    (the peer-memory sharded engine, see rgdbek_peer_connect / rgdbek_group_create).
+ *    z (local rows) is sharded.  Results are identical on every rank.
  *  - No CPU fallback exists: without a usable sm_100 GPU create() fails with
  *    RGDBEK_E_CUDA.
  */
@@ -56,6 +57,9 @@ extern "C" {
 #define RGDBEK_ABI_VERSION 1
 
 typedef struct rgdbek_ctx* rgdbek_handle;
+typedef struct rgdbek_group_s* rgdbek_group;    /* emulated ranks on one GPU (peer-sharded) */
+#define RGDBEK_PEER_HANDLE_BYTES 64             /* cudaIpcMemHandle_t */
+#define RGDBEK_MAX_PEER_RANKS 8
 
 typedef enum {
   RGDBEK_OK = 0,
@@ -250,6 +254,55 @@ int32_t       rgdbek_build_info(int32_t* out, int32_t max_entries);
 
 /* The cudaStream_t the handle runs on (for events / synchronisation). */
 void*         rgdbek_stream(rgdbek_handle h);
+
+/* ---------------------------------------------------------------------------------------
+ * Peer-memory sharded engine: Algorithm 1 row-sharded over R
+ * ranks as ONE persistent kernel per rank, ranks exchanging through peer memory (NVLink P2P
+ * loads / stores and release/acquire flag words), no NCCL calls.  A rank is a handle created
+ * with a partial row range [row_begin, row_end) and NO options.nccl_comm; global m, n, GLOBAL
+ * column ids.  Rank r's rows touch the column window W_r (min .. max column of its rows; all
+ * columns for dense A); every column is owned by one rank (rgdbek_plan_ownership), whose
+ * copy of s = A^T z (summed over the ranks whose window holds the column), keys, zeta and x
+ * is authoritative; the non-owned window columns of zeta and x (the halo) are read from
+ * their owners each iteration.  Trajectories do not depend on R (global Philox indices).
+ * Supported: the pseudoinverse-free update, random selection (RGDBEK_E_STATE otherwise).
+ * Sharded get_x gathers the owned parts of every rank; get_z is the rank's rows; get_blocks
+ * index lists are the rank's OWNED columns of U and its rows of J.
+ * ------------------------------------------------------------------------------------- */
+
+/* Owned-column boundaries for R ranks whose windows are windows[2r], windows[2r+1]
+ * (half-open): owned_bounds[0..R], owned_bounds[0] = 0, owned_bounds[R] = n.  Window
+ * starts and ends strictly increasing in r (banded A): each boundary splits the overlap of
+ * neighbouring windows at its midpoint (the halo exchange is then the overlap); otherwise
+ * (e.g. dense A, every window [0, n)) equal column slices.
+ * Host-only (no device needed). */
+rgdbek_status rgdbek_plan_ownership(int32_t nranks, const int64_t* windows, int64_t n,
+                                    int64_t* owned_bounds);
+
+/* out4 = {window begin, window end, first global row, one past the last row} of a rank. */
+rgdbek_status rgdbek_peer_window(rgdbek_handle h, int64_t* out4);
+
+/* R ranks on ONE GPU (emulated multi-GPU, e.g. for P-invariance tests): handles[r] are the
+ * ranks in row order (contiguous ranges covering [0, m), same device, m, n, storage).  The
+ * group runs ONE cooperative launch of R x G CTAs (G = SMs / R), so ranks that wait on one
+ * another are co-resident.  While grouped, rgdbek_step / rgdbek_solve on a member return
+ * RGDBEK_E_STATE; the per-rank getters work as documented above. */
+rgdbek_status rgdbek_group_create(rgdbek_group* out, const rgdbek_handle* handles, int32_t nranks);
+rgdbek_status rgdbek_group_reset(rgdbek_group g, uint64_t seed);
+rgdbek_status rgdbek_group_step(rgdbek_group g, int64_t n_iter, rgdbek_result* result);
+rgdbek_status rgdbek_group_solve(rgdbek_group g, double tol, int64_t max_iter, uint64_t seed,
+                                 rgdbek_result* result);
+void          rgdbek_group_destroy(rgdbek_group g);
+
+/* R real GPUs, one process per GPU: every rank exports its exchange block
+ * (RGDBEK_PEER_HANDLE_BYTES, a CUDA IPC handle), the caller allgathers the handles and the
+ * windows (rgdbek_peer_window) over its process group, and every rank calls
+ * rgdbek_peer_connect with them (handles: nranks x RGDBEK_PEER_HANDLE_BYTES, windows:
+ * 2 x nranks).  Afterwards rgdbek_step / rgdbek_solve are collectives: every rank must make
+ * the same call (its kernel waits on the others' flag words). */
+rgdbek_status rgdbek_peer_export(rgdbek_handle h, void* out_handle);
+rgdbek_status rgdbek_peer_connect(rgdbek_handle h, int32_t nranks, int32_t rank,
+                                  const void* handles, const int64_t* windows);
 
 /* NCCL bootstrap helpers (rank 0 makes the id; it is broadcast by the caller). */
 rgdbek_status rgdbek_nccl_unique_id(void* out_128_bytes);

@@ -13,7 +13,7 @@ from . import _native as N
 from ._native import (RgdbekError, RGDBEK_CONVERGED, RGDBEK_MAX_ITER, RGDBEK_STALLED,
                       RGDBEK_STOP_RSE, RGDBEK_STOP_REL_ERR, RGDBEK_STOP_NONE)
 
-__all__ = ["Solver", "RgdbekError", "RGDBEK_CONVERGED", "RGDBEK_MAX_ITER", "RGDBEK_STALLED",
+__all__ = ["Solver", "ShardGroup", "RgdbekError", "RGDBEK_CONVERGED", "RGDBEK_MAX_ITER", "RGDBEK_STALLED",
            "RGDBEK_STOP_RSE", "RGDBEK_STOP_REL_ERR", "RGDBEK_STOP_NONE", "library_path"]
 
 library_path = N.LIB_PATH
@@ -174,6 +174,10 @@ class Solver:
         (lazily averaged x-update); 0 returns to Algorithm 1."""
         N.rgdbek_set_lazy(self._h, int(processes))
 
+    def peer_window(self):
+        """(window begin, window end, first row, end row) of a peer-sharded rank."""
+        return tuple(N.rgdbek_peer_window(self._h))
+
     def passes(self):
         """Full passes over A since the last reset (persistent engine)."""
         return N.rgdbek_get_counters(self._h)
@@ -193,6 +197,37 @@ class Solver:
         if self._h:
             N.rgdbek_destroy(self._h)
             self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class ShardGroup:
+    """R peer-sharded ranks (Solvers created with row_range=..., m=..., no nccl_comm) on ONE
+    GPU, run as one cooperative launch (rgdbek_group_create): the multi-GPU decomposition
+    emulated for tests.  Per-rank state stays readable through the member Solvers."""
+
+    def __init__(self, solvers):
+        self.solvers = list(solvers)
+        self._g = N.rgdbek_group_create([s._h for s in self.solvers])
+
+    def reset(self, seed=0):
+        N.rgdbek_group_reset(self._g, int(seed), self.solvers[0]._h)
+
+    def step(self, n_iter):
+        return _res(N.rgdbek_group_step(self._g, int(n_iter), self.solvers[0]._h))
+
+    def solve(self, tol=1e-6, max_iter=100000, seed=0):
+        return _res(N.rgdbek_group_solve(self._g, float(tol), int(max_iter), int(seed),
+                                         self.solvers[0]._h))
+
+    def close(self):
+        if self._g:
+            N.rgdbek_group_destroy(self._g)
+            self._g = None
 
     def __del__(self):
         try:

@@ -24,7 +24,9 @@ EXPORTED = [
     "rgdbek_launch_kernel", "rgdbek_launches_per_iteration", "rgdbek_stream",
     "rgdbek_phase_times", "rgdbek_engine_info", "rgdbek_set_mode", "rgdbek_get_counters",
     "rgdbek_set_selection", "rgdbek_set_lazy", "rgdbek_set_capture", "rgdbek_selection_stats",
-    "rgdbek_build_info",
+    "rgdbek_build_info", "rgdbek_plan_ownership", "rgdbek_peer_window", "rgdbek_group_create",
+    "rgdbek_group_reset", "rgdbek_group_step", "rgdbek_group_solve", "rgdbek_group_destroy",
+    "rgdbek_peer_export", "rgdbek_peer_connect",
     "rgdbek_nccl_unique_id", "rgdbek_nccl_comm_init", "rgdbek_nccl_comm_destroy",
     "rgdbek_last_error", "rgdbek_destroy",
 ]
@@ -103,6 +105,17 @@ def load(path=None):
         "rgdbek_set_capture": (C.c_int, [H, C.c_int32]),
         "rgdbek_selection_stats": (C.c_int, [H, C.POINTER(C.c_int64)]),
         "rgdbek_build_info": (C.c_int32, [C.POINTER(C.c_int32), C.c_int32]),
+        "rgdbek_plan_ownership": (C.c_int, [C.c_int32, C.POINTER(C.c_int64), C.c_int64,
+                                            C.POINTER(C.c_int64)]),
+        "rgdbek_peer_window": (C.c_int, [H, C.POINTER(C.c_int64)]),
+        "rgdbek_group_create": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int32]),
+        "rgdbek_group_reset": (C.c_int, [C.c_void_p, C.c_uint64]),
+        "rgdbek_group_step": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(rgdbek_result)]),
+        "rgdbek_group_solve": (C.c_int, [C.c_void_p, C.c_double, C.c_int64, C.c_uint64,
+                                         C.POINTER(rgdbek_result)]),
+        "rgdbek_group_destroy": (None, [C.c_void_p]),
+        "rgdbek_peer_export": (C.c_int, [H, P]),
+        "rgdbek_peer_connect": (C.c_int, [H, C.c_int32, C.c_int32, P, C.POINTER(C.c_int64)]),
         "rgdbek_nccl_unique_id": (C.c_int, [P]),
         "rgdbek_nccl_comm_init": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, P,
                                             C.c_int32]),
@@ -255,6 +268,63 @@ def rgdbek_build_info():
     keys = ["tile_nnz", "tile_rows", "local_sel_max", "lcand_cap", "cand_cap", "final_cap",
             "persistent_threads", "tile_group_threads"]
     return dict(zip(keys, [buf[i] for i in range(cnt)]))
+
+
+PEER_HANDLE_BYTES = 64
+
+
+def rgdbek_plan_ownership(windows, n):
+    """Owned-column boundaries [R + 1] for rank windows [(lo, hi), ...] (host-only call)."""
+    R = len(windows)
+    w = (C.c_int64 * (2 * R))(*[int(v) for lohi in windows for v in lohi])
+    ob = (C.c_int64 * (R + 1))()
+    check(load().rgdbek_plan_ownership(R, w, int(n), ob), None)
+    return [ob[i] for i in range(R + 1)]
+
+
+def rgdbek_peer_window(h):
+    out = (C.c_int64 * 4)()
+    check(load().rgdbek_peer_window(h, out), h)
+    return [out[i] for i in range(4)]
+
+
+def rgdbek_group_create(handles):
+    arr = (C.c_void_p * len(handles))(*[h.value if isinstance(h, C.c_void_p) else h for h in handles])
+    g = C.c_void_p()
+    check(load().rgdbek_group_create(C.byref(g), arr, len(handles)), None)
+    return g
+
+
+def rgdbek_group_reset(g, seed, h0=None):
+    check(load().rgdbek_group_reset(g, seed), h0)
+
+
+def rgdbek_group_step(g, n_iter, h0=None):
+    r = rgdbek_result()
+    check(load().rgdbek_group_step(g, n_iter, C.byref(r)), h0)
+    return r
+
+
+def rgdbek_group_solve(g, tol, max_iter, seed, h0=None):
+    r = rgdbek_result()
+    check(load().rgdbek_group_solve(g, tol, max_iter, seed, C.byref(r)), h0)
+    return r
+
+
+def rgdbek_group_destroy(g):
+    load().rgdbek_group_destroy(g)
+
+
+def rgdbek_peer_export(h):
+    buf = (C.c_char * PEER_HANDLE_BYTES)()
+    check(load().rgdbek_peer_export(h, buf), h)
+    return bytes(buf)
+
+
+def rgdbek_peer_connect(h, nranks, rank, handles, windows):
+    hb = (C.c_char * (PEER_HANDLE_BYTES * nranks)).from_buffer_copy(b"".join(handles))
+    w = (C.c_int64 * (2 * nranks))(*[int(v) for lohi in windows for v in lohi])
+    check(load().rgdbek_peer_connect(h, nranks, rank, hb, w), h)
 
 
 def rgdbek_get_counters(h):

@@ -87,6 +87,10 @@ struct Scal {
   // selections whose level-1 bucket overflowed the shared-memory list, [1] selections
   // resolved by the persistent slow path, [2] by the graph engine's k_select_slow
   long long selstat[4];
+  // peer-memory sharded engine (sharded.cuh): exchange counter (identical on every rank,
+  // persists across launches with the flag words) and the combined ||b||^2
+  unsigned int xgen, pad3;
+  double bnorm2_global;
 };
 
 constexpr int SURV_CAP = 256;    // per-rank survivors exchanged by allgather

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "exact.cuh"
+#include "sharded.cuh"
 
 using namespace rg;
 
@@ -116,6 +117,23 @@ struct rgdbek_ctx {
   bool use_cond = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   long long launches_per_iter = 0;
+  // peer-memory sharded engine (sharded.cuh): a partial row range without an NCCL
+  // communicator.  The handle joins an emulated group on one GPU (rgdbek_group_create) or
+  // R real GPUs (rgdbek_peer_export / rgdbek_peer_connect).
+  bool peer = false;
+  long long wlo = 0, whi = 0;           // column window of the local rows
+  void* arena = nullptr;                // peer-visible block: s|v|X, zeta, x, XFlags, XPub[2]
+  size_t arena_bytes = 0;
+  size_t off_s = 0, off_zeta = 0, off_x = 0, off_flags = 0, off_pub = 0, off_gamma = 0;
+  XFlags* xflags = nullptr;
+  XPub* xpub = nullptr;
+  XComb* xcomb = nullptr;
+  ShArgs sh{};                          // this rank's view of the group
+  bool connected = false;               // real multi-GPU peers mapped (rgdbek_peer_connect)
+  struct rgdbek_group_s* group = nullptr;
+  void* ipc_open[MAXR] = {};            // peer arenas opened by cudaIpcOpenMemHandle
+  PArgs* d_pa = nullptr;                // device copies for the sharded launch
+  ShArgs* d_sa = nullptr;
   // errors
   int sticky = 0;
   std::string err;
@@ -281,6 +299,19 @@ __global__ void k_gather_csc(const int* perm, const int* row_of, const double* v
   }
 }
 
+__global__ void k_col_minmax(const int* ci, long long nnz, long long* mm /* [min, max] */) {
+  long long lo = 0x7FFFFFFFFFFFFFFFll, hi = -1;
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+       p += (long long)gridDim.x * blockDim.x) {
+    lo = min(lo, (long long)ci[p]);
+    hi = max(hi, (long long)ci[p]);
+  }
+  if (hi >= 0) {
+    atomicMin((unsigned long long*)&mm[0], (unsigned long long)lo);
+    atomicMax(&mm[1], hi);
+  }
+}
+
 __global__ void k_compare(const long long* a, const long long* b, long long n1, const int* c,
                           const int* d, const double* e, const double* f, long long n2,
                           int* flag) {
@@ -291,18 +322,20 @@ __global__ void k_compare(const long long* a, const long long* b, long long n1, 
   }
 }
 
-// Greedy row tiles: consecutive rows with <= TILE_NNZ nonzeros and <= TILE_ROWS rows
-// (a longer row is a tile by itself).
-rgdbek_status build_tiles(rgdbek_ctx* h, const long long* d_ptr, long long rows, int** out,
-                          long long** outp, int* nt) {
-  std::vector<long long> rp(rows + 1);
-  CK(h, cudaMemcpyAsync(rp.data(), d_ptr, (rows + 1) * sizeof(long long), cudaMemcpyDeviceToHost,
-                        h->stream));
+// Greedy row tiles over rows [r_begin, r_end): consecutive rows with <= TILE_NNZ nonzeros
+// and <= TILE_ROWS rows (a longer row is a tile by itself).  Tile ids are absolute rows.
+rgdbek_status build_tiles(rgdbek_ctx* h, const long long* d_ptr, long long r_begin, long long r_end,
+                          int** out, long long** outp, int* nt) {
+  const long long rows = r_end - r_begin;
+  std::vector<long long> rpv(rows + 1);
+  CK(h, cudaMemcpyAsync(rpv.data(), d_ptr + r_begin, (rows + 1) * sizeof(long long),
+                        cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
+  const long long* rp = rpv.data() - r_begin;          // rp[r] for r in [r_begin, r_end]
   std::vector<int> t;
-  t.push_back(0);
-  long long start = 0, acc = 0;
-  for (long long r = 0; r < rows; ++r) {
+  t.push_back((int)r_begin);
+  long long start = r_begin, acc = 0;
+  for (long long r = r_begin; r < r_end; ++r) {
     const long long len = rp[r + 1] - rp[r];
     if (r > start && (acc + len > TILE_NNZ || r - start >= TILE_ROWS)) {
       t.push_back((int)r);
@@ -311,7 +344,7 @@ rgdbek_status build_tiles(rgdbek_ctx* h, const long long* d_ptr, long long rows,
     }
     acc += len;
   }
-  t.push_back((int)rows);
+  if (rows > 0) t.push_back((int)r_end);
   std::vector<long long> tp(t.size());
   for (size_t i = 0; i < t.size(); ++i) tp[i] = rp[t[i]];
   int* d = nullptr;
@@ -732,6 +765,7 @@ void setup_l2_window(rgdbek_ctx* h) {
 }
 
 rgdbek_status finish_create(rgdbek_ctx* h) {
+  if (h->dense) { h->wlo = 0; h->whi = h->n; }     // dense rows touch every column
   // norms of b, block sizes (reading R2), scalar state, graph
   std::vector<double> hb(h->m_loc);
   CK(h, cudaMemcpyAsync(hb.data(), h->b, h->m_loc * sizeof(double), cudaMemcpyDeviceToHost,
@@ -751,7 +785,9 @@ rgdbek_status finish_create(rgdbek_ctx* h) {
     if (h->nccl_fail) return set_err(h, RGDBEK_E_NCCL, "ncclAllReduce failed at create");
   }
   h->bnorm2 = bn;
-  if (!(bn > 0.0)) return set_err(h, RGDBEK_E_ZERO_RHS, "||b|| == 0: RSE is undefined (P:301-304)");
+  // a peer-sharded rank may hold a zero part of b; ||b||^2 is summed over ranks on the device
+  if (!(bn > 0.0) && !h->peer)
+    return set_err(h, RGDBEK_E_ZERO_RHS, "||b|| == 0: RSE is undefined (P:301-304)");
   TRY(dalloc(h, &h->st, 1));
   CK(h, cudaMallocHost(&h->st_host, sizeof(Scal)));
   memset(h->st_host, 0, sizeof(Scal));
@@ -783,12 +819,38 @@ rgdbek_status alloc_vectors(rgdbek_ctx* h) {
   const long long n = h->n, m = h->m_loc;
   TRY(dalloc(h, &h->b, m));
   TRY(dalloc(h, &h->rho, m));
-  TRY(dalloc(h, &h->gamma, n));
-  TRY(dalloc(h, &h->x, n));
-  TRY(dalloc(h, &h->s, 2 * n + 1));      // [s | v | X]: one buffer for the sharded allreduce
+  if (!h->peer) TRY(dalloc(h, &h->gamma, n));           // peer ranks: in the arena
+  if (h->peer) {
+    // one peer-visible allocation (exported whole by CUDA IPC): the vectors peers read,
+    // the flag words they write and the publish blocks they read
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    h->off_s = 0;
+    h->off_zeta = up((size_t)(2 * n + 1) * sizeof(double) + 64);
+    h->off_x = h->off_zeta + up((size_t)n * sizeof(double) + 64);
+    h->off_flags = h->off_x + up((size_t)n * sizeof(double) + 64);
+    h->off_pub = h->off_flags + up(sizeof(XFlags));
+    h->off_gamma = h->off_pub + up(2 * sizeof(XPub));
+    h->arena_bytes = h->off_gamma + up((size_t)n * sizeof(double) + 64);
+    cudaError_t e = cudaMalloc(&h->arena, h->arena_bytes);
+    if (e != cudaSuccess) return set_err(h, RGDBEK_E_OOM, "cudaMalloc(arena) failed: %s", cudaGetErrorString(e));
+    h->allocs.push_back(h->arena);
+    CK(h, cudaMemsetAsync(h->arena, 0, h->arena_bytes, h->stream));
+    char* base = static_cast<char*>(h->arena);
+    h->s = reinterpret_cast<double*>(base + h->off_s);
+    h->zeta = reinterpret_cast<double*>(base + h->off_zeta);
+    h->x = reinterpret_cast<double*>(base + h->off_x);
+    h->xflags = reinterpret_cast<XFlags*>(base + h->off_flags);
+    h->xpub = reinterpret_cast<XPub*>(base + h->off_pub);
+    h->gamma = reinterpret_cast<double*>(base + h->off_gamma);
+    TRY(dalloc(h, &h->xcomb, 1));
+    CK(h, cudaMemsetAsync(h->xcomb, 0, sizeof(XComb), h->stream));
+  } else {
+    TRY(dalloc(h, &h->x, n));
+    TRY(dalloc(h, &h->s, 2 * n + 1));      // [s | v | X]: one buffer for the sharded allreduce
+    TRY(dalloc(h, &h->zeta, n));
+  }
   h->v = h->s + n;
   h->xslot = h->s + 2 * n;
-  TRY(dalloc(h, &h->zeta, n));
   TRY(dalloc(h, &h->xstar, n));
   TRY(dalloc(h, &h->z, m));
   TRY(dalloc(h, &h->w, m));
@@ -833,8 +895,10 @@ rgdbek_status common_begin(rgdbek_ctx* h, long long m, long long n, const rgdbek
   h->nccl = o->nccl_comm;
   h->trace_cap = std::max(0, o->trace_capacity);
   h->symmetric = o->symmetric != 0;
-  if (!h->nccl && (rb != 0 || re != m))
-    return set_err(h, RGDBEK_E_ARG, "a partial row range needs options.nccl_comm");
+  // a partial row range without an NCCL communicator: a rank of the peer-memory sharded
+  // engine (rgdbek_group_create on one GPU, rgdbek_peer_connect across GPUs)
+  h->peer = !h->nccl && (rb != 0 || re != m);
+  if (h->peer) h->symmetric = false;       // a row shard's CSC is not its CSR
   if (h->nccl) {
     NcclApi& api = nccl_api();
     if (!api.ok) return set_err(h, RGDBEK_E_NCCL, "libnccl.so.2 not loadable");
@@ -931,7 +995,104 @@ rgdbek_status ensure_usable(rgdbek_ctx* h) {
   return RGDBEK_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Peer-memory sharded engine (sharded.cuh): ownership, group setup, launch
+// ---------------------------------------------------------------------------
+// Owned-column boundaries conformal to the ranks' windows (rgdbek_plan_ownership).
+void plan_ownership(int R, const long long* win, long long n, long long* ob) {
+  // banded: window starts and ends strictly increasing with the rank (rows in order)
+  bool mono = true;
+  for (int r = 1; r < R; ++r)
+    if (win[2 * r] <= win[2 * (r - 1)] || win[2 * r + 1] <= win[2 * (r - 1) + 1]) mono = false;
+  ob[0] = 0;
+  ob[R] = n;
+  for (int r = 1; r < R; ++r) {
+    long long b;
+    if (mono) {
+      // banded: split the overlap of neighbouring windows at its midpoint, so every owned
+      // column lies in its owner's window and the halo is half the overlap on each side
+      b = (win[2 * r] + win[2 * (r - 1) + 1]) / 2;
+      // empty windows (no local nonzeros) own nothing
+      if (win[2 * r + 1] <= win[2 * r]) b = win[2 * (r - 1) + 1];
+    } else {
+      b = n * r / R;                     // unstructured: equal column slices
+    }
+    b = std::max(b, ob[r - 1]);
+    b = std::min(b, n);
+    ob[r] = b;
+  }
+}
+
+// gamma_j = sum over the ranks whose window holds j of their partial column norms
+// (P:94), for the owned columns of one rank; peers' partials are read in place.
+__global__ void k_gamma_combine(double* gamma, ShArgs x, const double* const* pg) {
+  for (long long j = x.own0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; j < x.own1;
+       j += (long long)gridDim.x * blockDim.x) {
+    double t = 0.0;
+    for (int r = 0; r < x.R; ++r)
+      if (j >= x.plo[r] && j < x.phi[r]) t += __ldcv(pg[r] + j);
+    gamma[j] = t;
+  }
+}
+
+size_t sharded_smem(const rgdbek_ctx* h) { return h->p_dyn; }
+
+rgdbek_status sharded_attr(rgdbek_ctx* h) {
+  const void* kf = h->dense ? (const void*)k_sharded<true> : (const void*)k_sharded<false>;
+  CK(h, cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sharded_smem(h)));
+  int occ = 0;
+  CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, PT, sharded_smem(h)));
+  if (occ < 1) return set_err(h, RGDBEK_E_CUDA, "sharded kernel cannot be resident");
+  return RGDBEK_OK;
+}
+
+// Fill this rank's ShArgs (everything except the peer pointer tables).
+void sharded_fill(rgdbek_ctx* h, int R, int rank, const long long* win, const long long* ob) {
+  ShArgs& x = h->sh;
+  memset(&x, 0, sizeof x);
+  x.R = R; x.rank = rank;
+  for (int r = 0; r <= R; ++r) x.ownb[r] = ob[r];
+  for (int r = 0; r < R; ++r) { x.plo[r] = win[2 * r]; x.phi[r] = win[2 * r + 1]; }
+  x.own0 = ob[rank]; x.own1 = ob[rank + 1];
+  x.wlo = h->wlo; x.whi = h->whi;
+  x.comb = h->xcomb;
+  x.bar = h->pbar;
+}
+
+// Pointers into a rank's arena at `base` (its own or an opened peer mapping).
+void sharded_peer(ShArgs& x, int r, const rgdbek_ctx* h, char* base) {
+  x.ps[r] = reinterpret_cast<double*>(base + h->off_s);
+  x.pv[r] = x.ps[r] + h->n;
+  x.pzeta[r] = reinterpret_cast<double*>(base + h->off_zeta);
+  x.px[r] = reinterpret_cast<double*>(base + h->off_x);
+  x.pflags[r] = reinterpret_cast<XFlags*>(base + h->off_flags);
+  x.ppub[r] = reinterpret_cast<XPub*>(base + h->off_pub);
+}
+
+const double* arena_gamma(const rgdbek_ctx* h, char* base) {
+  return reinterpret_cast<const double*>(base + h->off_gamma);
+}
+
+rgdbek_status fill_result(rgdbek_ctx* h, rgdbek_result* res, float ms);
+
 rgdbek_status run_loop(rgdbek_ctx* h, rgdbek_result* res) {
+  if (h->peer) {
+    // one rank of R real GPUs: this process's share of the sharded kernel (grid (G, 1));
+    // every rank must make the same call (a collective, like NCCL)
+    if (!h->connected) return set_err(h, RGDBEK_E_STATE, "peer-sharded rank: rgdbek_peer_connect first");
+    CK(h, cudaMemcpyAsync(h->d_pa, &h->pargs, sizeof(PArgs), cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(h->d_sa, &h->sh, sizeof(ShArgs), cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaEventRecord(h->ev0, h->stream));
+    void* args[] = {(void*)&h->d_pa, (void*)&h->d_sa};
+    const void* kf = h->dense ? (const void*)k_sharded<true> : (const void*)k_sharded<false>;
+    CK(h, cudaLaunchCooperativeKernel(kf, dim3(h->pG, 1), dim3(PT), args, sharded_smem(h), h->stream));
+    CK(h, cudaEventRecord(h->ev1, h->stream));
+    CK(h, cudaMemcpyAsync(h->st_host, h->st, sizeof(Scal), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    float ms = 0.f;
+    CK(h, cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    return fill_result(h, res, ms);
+  }
   CK(h, cudaEventRecord(h->ev0, h->stream));
   if (h->engine != 0) TRY(ensure_graph(h));
   if (h->engine == 0) {
@@ -960,6 +1121,10 @@ rgdbek_status run_loop(rgdbek_ctx* h, rgdbek_result* res) {
   CK(h, cudaStreamSynchronize(h->stream));
   float ms = 0.f;
   CK(h, cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  return fill_result(h, res, ms);
+}
+
+rgdbek_status fill_result(rgdbek_ctx* h, rgdbek_result* res, float ms) {
   const Scal& s = *h->st_host;
   if (s.error)
     return set_err(h, RGDBEK_E_INTERNAL, "device self-check failed (code %d): block size mismatch", s.error);
@@ -1012,6 +1177,7 @@ void rgdbek_destroy(rgdbek_handle h) {
     cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &v);
     cudaCtxResetPersistingL2Cache();
   }
+  for (int q = 0; q < MAXR; ++q) if (h->ipc_open[q]) cudaIpcCloseMemHandle(h->ipc_open[q]);
   if (h->exec) cudaGraphExecDestroy(h->exec);
   if (h->graph) cudaGraphDestroy(h->graph);
   if (h->body_exec) cudaGraphExecDestroy(h->body_exec);
@@ -1155,10 +1321,24 @@ rgdbek_status rgdbek_create_csr(rgdbek_handle* out, int64_t m, int64_t n, int64_
     const int v = atoi(e);
     if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) h->vecN = h->vecT = v;
   }
-  if ((s = build_tiles(h, h->rp, h->m_loc, &h->tilesN, &h->tilepN, &h->ntilesN)) != RGDBEK_OK) return create_fail(h, s);
+  if ((s = build_tiles(h, h->rp, 0, h->m_loc, &h->tilesN, &h->tilepN, &h->ntilesN)) != RGDBEK_OK) return create_fail(h, s);
+  // the column window of the local rows: a peer-sharded rank's pass T tiles cover only it
+  h->wlo = 0; h->whi = h->n;
+  if (h->peer) {
+    long long* wmm = nullptr;
+    if ((s = dalloc(h, &wmm, 2)) != RGDBEK_OK) return create_fail(h, s);
+    const long long init[2] = {h->n, -1};
+    cudaMemcpyAsync(wmm, init, sizeof init, cudaMemcpyHostToDevice, h->stream);
+    k_col_minmax<<<nblocks(nnz_local, 256, 4096), 256, 0, h->stream>>>(h->ci, nnz_local, wmm);
+    long long mm[2];
+    cudaMemcpyAsync(mm, wmm, sizeof mm, cudaMemcpyDeviceToHost, h->stream);
+    if (cudaStreamSynchronize(h->stream) != cudaSuccess) { set_err(h, RGDBEK_E_CUDA, "window reduction failed"); return create_fail(h, RGDBEK_E_CUDA); }
+    h->wlo = mm[1] < 0 ? 0 : mm[0];
+    h->whi = mm[1] < 0 ? 0 : mm[1] + 1;
+  }
   if (h->cp == h->rp) {
     h->tilesT = h->tilesN; h->tilepT = h->tilepN; h->ntilesT = h->ntilesN;
-  } else if ((s = build_tiles(h, h->cp, h->n, &h->tilesT, &h->tilepT, &h->ntilesT)) != RGDBEK_OK) {
+  } else if ((s = build_tiles(h, h->cp, h->wlo, h->whi, &h->tilesT, &h->tilepT, &h->ntilesT)) != RGDBEK_OK) {
     return create_fail(h, s);
   }
   {
@@ -1213,6 +1393,7 @@ rgdbek_status rgdbek_set_reference(rgdbek_handle h, const double* xstar) {
 
 rgdbek_status rgdbek_step(rgdbek_handle h, int64_t n_iter, rgdbek_result* res) {
   TRY(ensure_usable(h));
+  if (h->group) return set_err(h, RGDBEK_E_STATE, "this rank belongs to an emulated group: use rgdbek_group_step");
   if (n_iter < 0) return set_err(h, RGDBEK_E_ARG, "n_iter < 0");
   k_call_begin<<<1, 1, 0, h->stream>>>(h->st, n_iter, 1, 0.0, RGDBEK_STOP_NONE);
   CK(h, cudaGetLastError());
@@ -1222,6 +1403,7 @@ rgdbek_status rgdbek_step(rgdbek_handle h, int64_t n_iter, rgdbek_result* res) {
 rgdbek_status rgdbek_solve(rgdbek_handle h, double tol, int64_t max_iter, uint64_t seed,
                            rgdbek_result* res) {
   TRY(ensure_usable(h));
+  if (h->group) return set_err(h, RGDBEK_E_STATE, "this rank belongs to an emulated group: use rgdbek_group_solve");
   if (!(tol > 0.0) && h->stop_mode != RGDBEK_STOP_NONE) return set_err(h, RGDBEK_E_ARG, "tol must be > 0");
   if (max_iter < 1) return set_err(h, RGDBEK_E_ARG, "max_iter must be >= 1");
   if (h->stop_mode == RGDBEK_STOP_REL_ERR && !h->has_ref)
@@ -1235,6 +1417,18 @@ rgdbek_status rgdbek_solve(rgdbek_handle h, double tol, int64_t max_iter, uint64
 rgdbek_status rgdbek_get_x(rgdbek_handle h, double* out) {
   TRY(ensure_usable(h));
   if (!out) return set_err(h, RGDBEK_E_ARG, "NULL out");
+  if (h->peer && (h->group || h->connected)) {
+    // x is authoritative on each rank's owned columns: gather them (peer reads)
+    const ShArgs& x = h->sh;
+    for (int q = 0; q < x.R; ++q) {
+      const long long c0 = x.ownb[q], c1 = x.ownb[q + 1];
+      if (c1 > c0)
+        CK(h, cudaMemcpyAsync(out + c0, x.px[q] + c0, (c1 - c0) * sizeof(double), cudaMemcpyDefault,
+                              h->stream));
+    }
+    CK(h, cudaStreamSynchronize(h->stream));
+    return RGDBEK_OK;
+  }
   CK(h, cudaMemcpyAsync(out, h->x, h->n * sizeof(double), cudaMemcpyDefault, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
   return RGDBEK_OK;
@@ -1271,8 +1465,11 @@ rgdbek_status rgdbek_get_blocks(rgdbek_handle h, int64_t* n_u, uint64_t* hash_u,
     CK(h, cudaMemcpy(mk.data(), h->selmask_n + par * h->n, h->n, cudaMemcpyDeviceToHost));
     std::vector<int32_t> out;
     for (long long j = 0; j < h->n; ++j) if (mk[j]) out.push_back((int32_t)j);
-    if ((long long)out.size() != t.kp)
+    if (h->peer) {
+      if (n_u) *n_u = (int64_t)out.size();               // this rank's owned columns of U
+    } else if ((long long)out.size() != t.kp) {
       return set_err(h, RGDBEK_E_INTERNAL, "captured U has %zu entries, trace says %lld", out.size(), t.kp);
+    }
     CK(h, cudaMemcpy(U, out.data(), out.size() * sizeof(int32_t), cudaMemcpyDefault));
   }
   if (J) {
@@ -1280,9 +1477,9 @@ rgdbek_status rgdbek_get_blocks(rgdbek_handle h, int64_t* n_u, uint64_t* hash_u,
     CK(h, cudaMemcpy(mk.data(), h->selmask_m + par * h->m_loc, h->m_loc, cudaMemcpyDeviceToHost));
     std::vector<int32_t> out;
     for (long long i = 0; i < h->m_loc; ++i) if (mk[i]) out.push_back((int32_t)(h->row0 + i));
-    if (!h->dist && (long long)out.size() != t.kpp)
+    if (!h->dist && !h->peer && (long long)out.size() != t.kpp)
       return set_err(h, RGDBEK_E_INTERNAL, "captured J has %zu entries, trace says %lld", out.size(), t.kpp);
-    if (n_j && h->dist) *n_j = (int64_t)out.size();        // this rank's rows of J
+    if (n_j && (h->dist || h->peer)) *n_j = (int64_t)out.size();   // this rank's rows of J
     CK(h, cudaMemcpy(J, out.data(), out.size() * sizeof(int32_t), cudaMemcpyDefault));
   }
   return RGDBEK_OK;
@@ -1371,6 +1568,8 @@ rgdbek_status rgdbek_phase_times(rgdbek_handle h, double* out_ns, int32_t max_ph
 
 rgdbek_status rgdbek_set_mode(rgdbek_handle h, int32_t mode, double inner_tol, int32_t inner_max) {
   TRY(ensure_usable(h));
+  if (mode != 0 && h->peer)
+    return set_err(h, RGDBEK_E_STATE, "the peer-sharded engine runs the pseudoinverse-free update");
   if (mode < 0 || mode > 1) return set_err(h, RGDBEK_E_ARG, "unknown update mode %d", mode);
   if (mode == 1 && h->lazyP)
     return set_err(h, RGDBEK_E_STATE, "Algorithm 2 (set_lazy) runs the pseudoinverse-free update only");
@@ -1397,7 +1596,7 @@ rgdbek_status rgdbek_set_mode(rgdbek_handle h, int32_t mode, double inner_tol, i
 rgdbek_status rgdbek_set_selection(rgdbek_handle h, int32_t selection) {
   TRY(ensure_usable(h));
   if (selection < 0 || selection > 1) return set_err(h, RGDBEK_E_ARG, "unknown selection rule %d", selection);
-  if (selection == 1 && (h->engine != 0 || h->dist))
+  if (selection == 1 && (h->engine != 0 || h->dist || h->peer))
     return set_err(h, RGDBEK_E_STATE, "greedy selection runs on the single-GPU persistent engine");
   if (selection == 1 && h->lazyP)
     return set_err(h, RGDBEK_E_STATE, "Algorithm 2 (set_lazy) samples its blocks (random selection only)");
@@ -1417,7 +1616,7 @@ rgdbek_status rgdbek_set_lazy(rgdbek_handle h, int32_t processes) {
     if (h->pG_base) h->pG = h->pG_base;
     return RGDBEK_OK;
   }
-  if (!h->dense || h->engine != 0 || h->dist)
+  if (!h->dense || h->engine != 0 || h->dist || h->peer)
     return set_err(h, RGDBEK_E_STATE, "Algorithm 2 runs on the single-GPU persistent engine, dense A");
   if (h->mode != 0 || h->pargs.greedy)
     return set_err(h, RGDBEK_E_STATE, "Algorithm 2 needs the pseudoinverse-free update and random selection");
@@ -1550,6 +1749,260 @@ rgdbek_status rgdbek_nccl_comm_init(void** comm_out, int32_t nranks, int32_t ran
   typedef int (*init_by_val_t)(void**, int, Id, int);
   auto f = (init_by_val_t)dlsym(lib, "ncclCommInitRank");
   if (!f || f(comm_out, nranks, id, rank) != 0) return set_err(nullptr, RGDBEK_E_NCCL, "ncclCommInitRank failed");
+  return RGDBEK_OK;
+}
+
+// ===========================================================================
+// Peer-memory sharded engine: ownership plan, emulated groups, real peers
+// ===========================================================================
+rgdbek_status rgdbek_plan_ownership(int32_t nranks, const int64_t* windows, int64_t n,
+                                    int64_t* owned_bounds) {
+  if (nranks < 1 || nranks > MAXR || !windows || !owned_bounds || n < 1)
+    return set_err(nullptr, RGDBEK_E_ARG, "rgdbek_plan_ownership: bad arguments");
+  std::vector<long long> w(2 * nranks), ob(nranks + 1);
+  for (int i = 0; i < 2 * nranks; ++i) w[i] = windows[i];
+  plan_ownership(nranks, w.data(), n, ob.data());
+  for (int i = 0; i <= nranks; ++i) owned_bounds[i] = ob[i];
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_peer_window(rgdbek_handle h, int64_t* out4) {
+  TRY(ensure_usable(h));
+  if (!out4) return set_err(h, RGDBEK_E_ARG, "NULL out");
+  out4[0] = h->wlo; out4[1] = h->whi; out4[2] = h->row0; out4[3] = h->row0 + h->m_loc;
+  return RGDBEK_OK;
+}
+
+}  // extern "C"
+
+struct rgdbek_group_s {
+  int R = 0, G = 0, dense = 0;
+  rgdbek_ctx* h[MAXR] = {};
+  PArgs* d_pa = nullptr;
+  ShArgs* d_sa = nullptr;
+  const double** d_pg = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+rgdbek_status group_fail(rgdbek_group_s* g, rgdbek_status st, const char* msg) {
+  set_err(nullptr, st, "%s", msg);
+  if (g) {
+    for (int r = 0; r < g->R; ++r) if (g->h[r]) g->h[r]->group = nullptr;
+    if (g->d_pa) cudaFree(g->d_pa);
+    if (g->d_sa) cudaFree(g->d_sa);
+    if (g->d_pg) cudaFree(g->d_pg);
+    if (g->ev0) cudaEventDestroy(g->ev0);
+    if (g->ev1) cudaEventDestroy(g->ev1);
+    delete g;
+  }
+  return st;
+}
+
+rgdbek_status group_run(rgdbek_group_s* g, rgdbek_result* res) {
+  rgdbek_ctx* h0 = g->h[0];
+  cudaStream_t st = h0->stream;
+  for (int r = 0; r < g->R; ++r) {
+    CK(h0, cudaMemcpyAsync(g->d_pa + r, &g->h[r]->pargs, sizeof(PArgs), cudaMemcpyHostToDevice, st));
+    CK(h0, cudaMemcpyAsync(g->d_sa + r, &g->h[r]->sh, sizeof(ShArgs), cudaMemcpyHostToDevice, st));
+  }
+  CK(h0, cudaEventRecord(g->ev0, st));
+  void* args[] = {(void*)&g->d_pa, (void*)&g->d_sa};
+  const void* kf = g->dense ? (const void*)k_sharded<true> : (const void*)k_sharded<false>;
+  CK(h0, cudaLaunchCooperativeKernel(kf, dim3(g->G, g->R), dim3(PT), args, sharded_smem(h0), st));
+  CK(h0, cudaEventRecord(g->ev1, st));
+  for (int r = 0; r < g->R; ++r)
+    CK(h0, cudaMemcpyAsync(g->h[r]->st_host, g->h[r]->st, sizeof(Scal), cudaMemcpyDeviceToHost, st));
+  CK(h0, cudaStreamSynchronize(st));
+  float ms = 0.f;
+  CK(h0, cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+  for (int r = 0; r < g->R; ++r) {
+    const Scal& a = *g->h[r]->st_host;
+    const Scal& b = *h0->st_host;
+    if (a.iters != b.iters || a.outcome != b.outcome)
+      return set_err(h0, RGDBEK_E_INTERNAL, "ranks disagree: rank %d stopped at %lld, rank 0 at %lld",
+                     r, a.iters, b.iters);
+    rgdbek_status s = fill_result(g->h[r], r == 0 ? res : nullptr, ms);
+    if (s != RGDBEK_OK) return set_err(h0, s, "rank %d: %s", r, g->h[r]->err.c_str());
+  }
+  return RGDBEK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+rgdbek_status rgdbek_group_create(rgdbek_group* out, const rgdbek_handle* handles, int32_t nranks) {
+  if (!out || !handles || nranks < 1 || nranks > MAXR)
+    return set_err(nullptr, RGDBEK_E_ARG, "rgdbek_group_create: need 1..%d handles", MAXR);
+  *out = nullptr;
+  rgdbek_group_s* g = new rgdbek_group_s();
+  g->R = nranks;
+  for (int r = 0; r < nranks; ++r) {
+    rgdbek_ctx* h = handles[r];
+    if (!h || h->sticky) return group_fail(g, RGDBEK_E_ARG, "NULL or failed handle");
+    g->h[r] = h;
+    if (!h->peer)
+      return group_fail(g, RGDBEK_E_STATE, "group ranks must be created with a partial row range "
+                                            "and no NCCL communicator");
+    if (h->group || h->connected) return group_fail(g, RGDBEK_E_STATE, "a handle is already grouped / connected");
+    if (h->mode != 0 || h->pargs.greedy || h->lazyP)
+      return group_fail(g, RGDBEK_E_STATE, "the sharded engine runs Algorithm 1 (pseudoinverse-free, random selection)");
+    const rgdbek_ctx* h0 = handles[0];
+    if (h->device != h0->device || h->n != h0->n || h->m != h0->m || h->dense != h0->dense)
+      return group_fail(g, RGDBEK_E_DIM, "group ranks must share device, m, n and storage kind");
+    const long long expect = r == 0 ? 0 : handles[r - 1]->row0 + handles[r - 1]->m_loc;
+    if (h->row0 != expect) return group_fail(g, RGDBEK_E_DIM, "row ranges must be contiguous, in rank order");
+    if (r == nranks - 1 && h->row0 + h->m_loc != h->m) return group_fail(g, RGDBEK_E_DIM, "row ranges must cover [0, m)");
+  }
+  rgdbek_ctx* h0 = g->h[0];
+  g->dense = h0->dense ? 1 : 0;
+  if (cudaSetDevice(h0->device) != cudaSuccess) return group_fail(g, RGDBEK_E_CUDA, "cudaSetDevice");
+  for (int r = 0; r < nranks; ++r)
+    if (cudaStreamSynchronize(g->h[r]->stream) != cudaSuccess) return group_fail(g, RGDBEK_E_CUDA, "stream sync");
+  // co-resident: R x G CTAs of one 1024-thread block per SM
+  if (sharded_attr(h0) != RGDBEK_OK) return group_fail(g, RGDBEK_E_CUDA, h0->err.c_str());
+  int nsm = 148, occ = 1;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h0->device);
+  const void* kf = g->dense ? (const void*)k_sharded<true> : (const void*)k_sharded<false>;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, PT, sharded_smem(h0));
+  int G = (nsm * std::max(occ, 1)) / nranks;
+  for (int r = 0; r < nranks; ++r) G = std::min(G, g->h[r]->pG);
+  if (const char* e = getenv("RGDBEK_GRID")) G = std::min(G, std::max(1, atoi(e)));
+  if (G < 1) return group_fail(g, RGDBEK_E_ARG, "too many ranks for one GPU");
+  g->G = G;
+  std::vector<long long> win(2 * nranks), ob(nranks + 1);
+  for (int r = 0; r < nranks; ++r) { win[2 * r] = g->h[r]->wlo; win[2 * r + 1] = g->h[r]->whi; }
+  plan_ownership(nranks, win.data(), h0->n, ob.data());
+  std::vector<const double*> pg(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    rgdbek_ctx* h = g->h[r];
+    sharded_fill(h, nranks, r, win.data(), ob.data());
+    for (int q = 0; q < nranks; ++q) sharded_peer(h->sh, q, g->h[q], static_cast<char*>(g->h[q]->arena));
+    pg[r] = arena_gamma(g->h[r], static_cast<char*>(g->h[r]->arena));
+  }
+  cudaStream_t st = h0->stream;
+  if (cudaMalloc(&g->d_pa, nranks * sizeof(PArgs)) != cudaSuccess ||
+      cudaMalloc(&g->d_sa, nranks * sizeof(ShArgs)) != cudaSuccess ||
+      cudaMalloc(&g->d_pg, nranks * sizeof(double*)) != cudaSuccess ||
+      cudaEventCreate(&g->ev0) != cudaSuccess || cudaEventCreate(&g->ev1) != cudaSuccess)
+    return group_fail(g, RGDBEK_E_OOM, "group buffers");
+  cudaMemcpyAsync(g->d_pg, pg.data(), nranks * sizeof(double*), cudaMemcpyHostToDevice, st);
+  // global column norms on the owned columns: sums of the ranks' partials
+  for (int r = 0; r < nranks; ++r)
+    k_gamma_combine<<<nblocks(std::max<long long>(1, g->h[r]->sh.own1 - g->h[r]->sh.own0), 256, 2048),
+                      256, 0, st>>>(g->h[r]->gamma, g->h[r]->sh, g->d_pg);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return group_fail(g, RGDBEK_E_CUDA, "gamma combine");
+  for (int r = 0; r < nranks; ++r) g->h[r]->group = g;
+  *out = g;
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_group_reset(rgdbek_group g, uint64_t seed) {
+  if (!g) return RGDBEK_E_ARG;
+  for (int r = 0; r < g->R; ++r) TRY(rgdbek_reset(g->h[r], seed));
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_group_step(rgdbek_group g, int64_t n_iter, rgdbek_result* res) {
+  if (!g) return RGDBEK_E_ARG;
+  rgdbek_ctx* h0 = g->h[0];
+  TRY(ensure_usable(h0));
+  if (n_iter < 0) return set_err(h0, RGDBEK_E_ARG, "n_iter < 0");
+  for (int r = 0; r < g->R; ++r) {
+    CK(h0, cudaStreamSynchronize(g->h[r]->stream));
+    k_call_begin<<<1, 1, 0, h0->stream>>>(g->h[r]->st, n_iter, 1, 0.0, RGDBEK_STOP_NONE);
+  }
+  CK(h0, cudaGetLastError());
+  return group_run(g, res);
+}
+
+rgdbek_status rgdbek_group_solve(rgdbek_group g, double tol, int64_t max_iter, uint64_t seed,
+                                 rgdbek_result* res) {
+  if (!g) return RGDBEK_E_ARG;
+  rgdbek_ctx* h0 = g->h[0];
+  TRY(ensure_usable(h0));
+  if (!(tol > 0.0) && h0->stop_mode != RGDBEK_STOP_NONE) return set_err(h0, RGDBEK_E_ARG, "tol must be > 0");
+  if (max_iter < 1) return set_err(h0, RGDBEK_E_ARG, "max_iter must be >= 1");
+  for (int r = 0; r < g->R; ++r) {
+    if (g->h[r]->stop_mode != h0->stop_mode) return set_err(h0, RGDBEK_E_ARG, "ranks disagree on the stop rule");
+    if (h0->stop_mode == RGDBEK_STOP_REL_ERR && !g->h[r]->has_ref)
+      return set_err(h0, RGDBEK_E_STATE, "STOP_REL_ERR needs rgdbek_set_reference on every rank");
+  }
+  TRY(rgdbek_group_reset(g, seed));
+  for (int r = 0; r < g->R; ++r)
+    k_call_begin<<<1, 1, 0, h0->stream>>>(g->h[r]->st, max_iter, 0, tol, h0->stop_mode);
+  CK(h0, cudaGetLastError());
+  return group_run(g, res);
+}
+
+void rgdbek_group_destroy(rgdbek_group g) {
+  if (!g) return;
+  cudaSetDevice(g->h[0]->device);
+  cudaStreamSynchronize(g->h[0]->stream);
+  for (int r = 0; r < g->R; ++r) g->h[r]->group = nullptr;
+  cudaFree(g->d_pa);
+  cudaFree(g->d_sa);
+  cudaFree(g->d_pg);
+  cudaEventDestroy(g->ev0);
+  cudaEventDestroy(g->ev1);
+  delete g;
+}
+
+// ---- R real GPUs: CUDA IPC of each rank's arena ----
+rgdbek_status rgdbek_peer_export(rgdbek_handle h, void* out_handle) {
+  TRY(ensure_usable(h));
+  if (!h->peer || !out_handle) return set_err(h, RGDBEK_E_STATE, "not a peer-sharded rank (partial row range, no NCCL)");
+  cudaIpcMemHandle_t ih;
+  CK(h, cudaIpcGetMemHandle(&ih, h->arena));
+  static_assert(sizeof(cudaIpcMemHandle_t) == RGDBEK_PEER_HANDLE_BYTES, "IPC handle size");
+  memcpy(out_handle, &ih, sizeof ih);
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_peer_connect(rgdbek_handle h, int32_t nranks, int32_t rank,
+                                  const void* handles, const int64_t* windows) {
+  TRY(ensure_usable(h));
+  if (!h->peer) return set_err(h, RGDBEK_E_STATE, "not a peer-sharded rank (partial row range, no NCCL)");
+  if (h->group || h->connected) return set_err(h, RGDBEK_E_STATE, "already grouped / connected");
+  if (nranks < 1 || nranks > MAXR || rank < 0 || rank >= nranks || !handles || !windows)
+    return set_err(h, RGDBEK_E_ARG, "rgdbek_peer_connect: bad arguments");
+  if (h->mode != 0 || h->pargs.greedy || h->lazyP)
+    return set_err(h, RGDBEK_E_STATE, "the sharded engine runs Algorithm 1 (pseudoinverse-free, random selection)");
+  std::vector<long long> win(2 * nranks), ob(nranks + 1);
+  for (int i = 0; i < 2 * nranks; ++i) win[i] = windows[i];
+  if (win[2 * rank] != h->wlo || win[2 * rank + 1] != h->whi)
+    return set_err(h, RGDBEK_E_ARG, "windows[rank] differs from this rank's window");
+  plan_ownership(nranks, win.data(), h->n, ob.data());
+  sharded_fill(h, nranks, rank, win.data(), ob.data());
+  std::vector<const double*> pg(nranks);
+  for (int q = 0; q < nranks; ++q) {
+    char* base;
+    if (q == rank) {
+      base = static_cast<char*>(h->arena);
+    } else {
+      cudaIpcMemHandle_t ih;
+      memcpy(&ih, static_cast<const char*>(handles) + (size_t)q * RGDBEK_PEER_HANDLE_BYTES, sizeof ih);
+      void* p = nullptr;
+      CK(h, cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess));
+      h->ipc_open[q] = p;
+      base = static_cast<char*>(p);
+    }
+    sharded_peer(h->sh, q, h, base);       // every rank has the same arena layout (same n)
+    pg[q] = arena_gamma(h, base);
+  }
+  TRY(sharded_attr(h));
+  const double** d_pg = nullptr;
+  TRY(dalloc(h, &d_pg, nranks));
+  TRY(dalloc(h, &h->d_pa, 1));
+  TRY(dalloc(h, &h->d_sa, 1));
+  CK(h, cudaMemcpyAsync(d_pg, pg.data(), nranks * sizeof(double*), cudaMemcpyHostToDevice, h->stream));
+  k_gamma_combine<<<nblocks(std::max<long long>(1, h->sh.own1 - h->sh.own0), 256, 2048), 256, 0,
+                    h->stream>>>(h->gamma, h->sh, d_pg);
+  CK(h, cudaGetLastError());
+  CK(h, cudaStreamSynchronize(h->stream));
+  h->connected = true;
   return RGDBEK_OK;
 }
 

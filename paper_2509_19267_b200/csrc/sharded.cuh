@@ -89,6 +89,19 @@ __device__ __forceinline__ unsigned int ld_acquire_sys_u32(const unsigned int* p
   return v;
 }
 
+// Watchdog of the cross-rank waits: a rank that never arrives (a bug, or a peer process
+// that died) traps the kernel after RG_XWAIT_NS instead of hanging the GPU.
+#ifndef RG_XWAIT_NS
+#define RG_XWAIT_NS 20000000000ull
+#endif
+__device__ __forceinline__ void x_watch(unsigned int& spins, unsigned long long& t0) {
+  if ((++spins & 1023u) == 0u) {
+    const unsigned long long t = gtimer();
+    if (t0 == 0ull) t0 = t;
+    else if (t - t0 > RG_XWAIT_NS) __trap();
+  }
+}
+
 // Signal round `rd` of exchange number `g` to every rank, then wait until every rank has.
 // Called by CTA 0 only, all threads.
 __device__ __forceinline__ void x_flags(const ShArgs& x, int rd, unsigned int g) {
@@ -97,7 +110,9 @@ __device__ __forceinline__ void x_flags(const ShArgs& x, int rd, unsigned int g)
   if (threadIdx.x < x.R) st_release_sys_u32(&x.pflags[threadIdx.x]->arrive[rd][x.rank], g);
   if (threadIdx.x < x.R) {
     const unsigned int* f = &x.pflags[x.rank]->arrive[rd][threadIdx.x];
-    while ((int)(ld_acquire_sys_u32(f) - g) < 0) { }
+    unsigned int spins = 0u;
+    unsigned long long t0 = 0ull;
+    while ((int)(ld_acquire_sys_u32(f) - g) < 0) x_watch(spins, t0);
   }
   __syncthreads();
 }
@@ -139,7 +154,9 @@ __device__ void xsync(const PArgs& a, const ShArgs& x, unsigned int& bgen, unsig
     if (threadIdx.x == 0) {
       bgen = myg + 1u;
       atom_add_acqrel_u32(&gb->count, 1u);
-      while (ld_acquire_u32(&gb->gen) == myg) { }
+      unsigned int spins = 0u;
+      unsigned long long t0 = 0ull;
+      while (ld_acquire_u32(&gb->gen) == myg) x_watch(spins, t0);
     }
     __syncthreads();
     return;
@@ -147,7 +164,9 @@ __device__ void xsync(const PArgs& a, const ShArgs& x, unsigned int& bgen, unsig
   // ---- CTA 0: wait for the rank's other CTAs ----
   if (threadIdx.x == 0) {
     bgen = myg + 1u;
-    while (ld_acquire_u32(&gb->count) != gridDim.x - 1) { }
+    unsigned int spins = 0u;
+    unsigned long long t0 = 0ull;
+    while (ld_acquire_u32(&gb->count) != gridDim.x - 1) x_watch(spins, t0);
     gb->count = 0u;
   }
   __syncthreads();

@@ -62,3 +62,19 @@ def init_nccl_comm(device, group=None):
 
 def destroy_nccl_comm(comm):
     N.rgdbek_nccl_comm_destroy(comm)
+
+
+def connect_peers(solver, group=None):
+    """Join this process's peer-sharded rank (a Solver created with row_range and no
+    nccl_comm) to the other ranks of the torch.distributed group: every rank exports its
+    exchange block (CUDA IPC handle) and window, the group allgathers them, and every rank
+    maps its peers (rgdbek_peer_connect).  Afterwards solver.step / solver.solve are
+    collectives over the group (one persistent kernel per GPU, peer-memory exchanges)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    mine = (N.rgdbek_peer_export(solver._h), tuple(solver.peer_window()[:2]))
+    allv = [None] * world
+    dist.all_gather_object(allv, mine, group=group)
+    N.rgdbek_peer_connect(solver._h, world, rank, [a[0] for a in allv], [a[1] for a in allv])
+    dist.barrier(group=group)

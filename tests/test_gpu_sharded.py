@@ -1,0 +1,162 @@
+"""Peer-memory sharded engine (sharded.cuh, SURVEY §8(e) banded / generic plan; pin P15):
+R ranks emulated on ONE GPU as one cooperative launch (rgdbek_group_create), each rank a
+handle over its nnz-balanced rows, exchanging only window partials, halos,
+histograms and scalars through peer memory.
+
+Bars: the trajectory does not depend on R (global Philox indices, reading R5): for
+R = 2, 4, 8 the FULL block index lists U_k, J_k equal the single-process oracle's every
+iteration, x and z within 1e-10 (reading R18), iterations to 1e-6 within 2 %.  This runs
+the code paths that only matter at R > 1: row0 > 0 Philox indexing, cross-rank histogram
+sums and survivor gathers, the owned-column reduce of window partials, the halo copy and
+the R-rank barrier.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2509_19267_b200 import _build
+    _build.build()
+
+
+def _group(w, R):
+    from paper_2509_19267_b200 import Solver, ShardGroup
+    from paper_2509_19267_b200.dist import partition_rows, shard_csr
+    m, n = w.shape
+    parts = partition_rows(m if w.dense else w.A.indptr, R)
+    ss = []
+    for (r0, r1) in parts:
+        if w.dense:
+            s = Solver(w.A[r0:r1], w.b[r0:r1], eta=w.eta, m=m, row_range=(r0, r1))
+        else:
+            rp, ci, val = shard_csr(*w.csr_arrays(), r0, r1)
+            s = Solver.from_csr(m, n, rp, ci, val, w.b[r0:r1], eta=w.eta, row_range=(r0, r1))
+        ss.append(s)
+    return ss, ShardGroup(ss), parts
+
+
+def _close(ss, g):
+    g.close()
+    for s in ss:
+        s.close()
+
+
+def _lists(ss):
+    U = np.concatenate([s.block_lists()[0] for s in ss])
+    J = np.concatenate([s.block_lists()[1] for s in ss])
+    return np.sort(U), np.sort(J)
+
+
+@pytest.mark.parametrize("R", [2, 4, 8])
+@pytest.mark.parametrize("name", ["C2si", "C5t", "C3s", "C1"])
+def test_p_invariant_trajectory(name, R):
+    from oracle import Oracle
+    from workloads import by_name
+    w = by_name(name)
+    ss, g, parts = _group(w, R)
+    for s in ss:
+        s.set_capture(True)
+    o = Oracle(w.A, w.b, w.eta)
+    g.reset(3)
+    bn = np.linalg.norm(w.b)
+    for k in range(20):
+        rec = o.iterate(3, keep_blocks=True)
+        g.step(1)
+        for s in ss:                                       # every rank traced the same globals
+            t = s.trace()[-1]
+            assert (t["k"], t["kp"], t["hash_u"], t["kpp"], t["hash_j"]) == \
+                   (k, rec.kp, rec.hash_u, rec.kpp, rec.hash_j), (k, s)
+        U, J = _lists(ss)
+        assert np.array_equal(U, rec.U), f"U differs at k={k}"
+        assert np.array_equal(J, rec.J), f"J differs at k={k}"
+        for s in ss:
+            assert np.linalg.norm(s.x() - o.x) <= 1e-10 * max(np.linalg.norm(o.x), 1e-300), k
+        z = np.concatenate([s.z() for s in ss])
+        assert np.linalg.norm(z - o.z) <= 1e-10 * bn, k
+    _close(ss, g)
+
+
+@pytest.mark.parametrize("R", [3, 8])
+def test_sharded_time_to_tolerance(R):
+    """C5t (the population-model twin): iterations to ||x - x*||/||x*|| <= 1e-6 within 2 %
+    of the oracle's at R ranks."""
+    from oracle import Oracle, STOP_REL_ERR
+    from paper_2509_19267_b200 import RGDBEK_CONVERGED
+    from workloads import by_name
+    w = by_name("C5t")
+    ss, g, _ = _group(w, R)
+    for s in ss:
+        s.set_stop("rel_err")
+        s.set_reference(w.xstar)
+    res = g.solve(1e-6, 100000, 0)
+    o = Oracle(w.A, w.b, w.eta)
+    out, iters, _, _ = o.solve(1e-6, 100000, 0, stop=STOP_REL_ERR, xstar=w.xstar)
+    assert res["outcome"] == RGDBEK_CONVERGED == out
+    assert abs(res["iters"] - iters) <= max(1, int(0.02 * iters)), (res["iters"], iters)
+    _close(ss, g)
+
+
+def test_sharded_small_grids_block_sizes_and_determinism(monkeypatch):
+    """2 CTAs per rank (cross-CTA paths), block size 1 and eta = 0.97 (SEL_ALL-type
+    selections), and two runs bitwise identical."""
+    from oracle import Oracle
+    from workloads import dense_gaussian
+    monkeypatch.setenv("RGDBEK_GRID", "2")
+    for eta in (0.001, 0.97):
+        w = dense_gaussian(300, 80, seed=2, noise=0.1)
+        w.eta = eta
+        ss, g, _ = _group(w, 4)
+        o = Oracle(w.A, w.b, eta)
+        g.reset(1)
+        for k in range(15):
+            rec = o.iterate(1)
+            g.step(1)
+            t = ss[0].trace()[-1]
+            assert (t["kp"], t["hash_u"], t["kpp"], t["hash_j"]) == (rec.kp, rec.hash_u, rec.kpp, rec.hash_j)
+        x1 = ss[0].x()
+        g.reset(1)
+        g.step(15)
+        assert np.array_equal(ss[0].x(), x1)
+        assert np.linalg.norm(x1 - o.x) <= 1e-10 * np.linalg.norm(o.x)
+        _close(ss, g)
+
+
+def test_sharded_step_chunks_and_stop_rules():
+    """Chunked steps equal one run; the RSE stop and MAX_ITER outcomes on every rank."""
+    from paper_2509_19267_b200 import RGDBEK_MAX_ITER
+    from workloads import by_name
+    w = by_name("C5t")
+    ss, g, _ = _group(w, 4)
+    g.reset(5)
+    g.step(9)
+    g.step(0)
+    g.step(6)
+    xa = ss[0].x()
+    g.reset(5)
+    r = g.step(15)
+    assert r["iters"] == 15 and np.array_equal(ss[0].x(), xa)
+    res = g.solve(1e-300, 7, 0)
+    assert res["outcome"] == RGDBEK_MAX_ITER and res["iters"] == 7
+    _close(ss, g)
+
+
+def test_group_argument_checks():
+    from paper_2509_19267_b200 import RgdbekError, Solver, ShardGroup
+    from workloads import by_name
+    w = by_name("C1")
+    a = Solver(w.A[:100], w.b[:100], m=200, row_range=(0, 100))
+    b = Solver(w.A[120:], w.b[120:], m=200, row_range=(120, 200))
+    with pytest.raises(RgdbekError):                     # rows 100..120 missing
+        ShardGroup([a, b])
+    with pytest.raises(RgdbekError):                     # a grouped rank cannot step alone
+        c = Solver(w.A[100:], w.b[100:], m=200, row_range=(100, 200))
+        g = ShardGroup([a, c])
+        try:
+            a.step(1)
+        finally:
+            g.close()
+    with pytest.raises(RgdbekError):
+        a.set_mode("exact")
