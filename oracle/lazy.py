@@ -52,12 +52,20 @@ def partition_bounds(m, P):
 class LazyOracle(Oracle):
     """Algorithm 2 with P logical processes, pinv-free reading R28."""
 
-    def __init__(self, A, b, eta=0.5, parts=2):
+    def __init__(self, A, b, eta=0.5, parts=2, bounds=None):
         super().__init__(A, b, eta)
+        if bounds is not None:
+            # explicit contiguous row blocks (e.g. the nnz-balanced ranks of P:443)
+            bounds = [(int(r0), int(r1)) for r0, r1 in bounds]
+            if bounds[0][0] != 0 or bounds[-1][1] != self.m or any(
+                    bounds[i][1] != bounds[i + 1][0] or bounds[i][0] >= bounds[i][1]
+                    for i in range(len(bounds) - 1)):
+                raise ValueError("bounds must be contiguous non-empty row blocks covering [0, m)")
+            parts = len(bounds)
         if not 1 <= parts <= self.m:
             raise ValueError("parts must lie in [1, m]")
         self.P = int(parts)
-        self.bounds = partition_bounds(self.m, self.P)
+        self.bounds = bounds if bounds is not None else partition_bounds(self.m, self.P)
 
     def column_step(self, seed):
         """global U from A^T z; a local first-CGLS z-step per process."""

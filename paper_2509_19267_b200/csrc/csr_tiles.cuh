@@ -47,6 +47,13 @@ namespace rg {
 #ifndef RG_TG
 #define RG_TG 256
 #endif
+#ifndef RG_RU5
+// gather entries per lane per round at 32 lanes per row (tiles of a few long rows, e.g. the
+// ~200-entry CSC columns of C5): 7 covers a 224-entry row in ONE round trip instead of
+// two (tools/ab_pass.py, profiles/r2/ab_pass_2.log: C5m pass T +13 %, iteration +8.6 %;
+// 8 the same, 6 = RG_RU the old default)
+#define RG_RU5 7
+#endif
 constexpr int TG = RG_TG;            // threads per worker group
 constexpr int TILE_NNZ = RG_TILE_NNZ;    // nonzeros per tile
 constexpr int TILE_ROWS = RG_TILE_ROWS;  // rows per tile
@@ -227,7 +234,7 @@ __device__ __forceinline__ void tile_rows(const TileRows& t, double& Wp, double&
       const int q1 = (int)(t.R[r + 1] - t.p0);
       // RU entries per lane per round, predicated: one gather round trip
       // covers a whole row of up to RU * v entries
-      constexpr int RU = RG_RU;
+      constexpr int RU = LV == 5 ? RG_RU5 : RG_RU;
       for (; q < q1; q += RU * v) {
         int c[RU];
         double g1[RU], g2[RU];

@@ -124,7 +124,7 @@ struct rgdbek_ctx {
   long long wlo = 0, whi = 0;           // column window of the local rows
   void* arena = nullptr;                // peer-visible block: s|v|X, zeta, x, XFlags, XPub[2]
   size_t arena_bytes = 0;
-  size_t off_s = 0, off_zeta = 0, off_x = 0, off_flags = 0, off_pub = 0, off_gamma = 0;
+  size_t off_s = 0, off_zeta = 0, off_x = 0, off_flags = 0, off_pub = 0, off_gamma = 0, off_keys = 0;
   XFlags* xflags = nullptr;
   XPub* xpub = nullptr;
   XComb* xcomb = nullptr;
@@ -830,7 +830,8 @@ rgdbek_status alloc_vectors(rgdbek_ctx* h) {
     h->off_flags = h->off_x + up((size_t)n * sizeof(double) + 64);
     h->off_pub = h->off_flags + up(sizeof(XFlags));
     h->off_gamma = h->off_pub + up(2 * sizeof(XPub));
-    h->arena_bytes = h->off_gamma + up((size_t)n * sizeof(double) + 64);
+    h->off_keys = h->off_gamma + up((size_t)n * sizeof(double) + 64);
+    h->arena_bytes = h->off_keys + up((size_t)n * sizeof(unsigned long long) + 64);
     cudaError_t e = cudaMalloc(&h->arena, h->arena_bytes);
     if (e != cudaSuccess) return set_err(h, RGDBEK_E_OOM, "cudaMalloc(arena) failed: %s", cudaGetErrorString(e));
     h->allocs.push_back(h->arena);
@@ -842,6 +843,7 @@ rgdbek_status alloc_vectors(rgdbek_ctx* h) {
     h->xflags = reinterpret_cast<XFlags*>(base + h->off_flags);
     h->xpub = reinterpret_cast<XPub*>(base + h->off_pub);
     h->gamma = reinterpret_cast<double*>(base + h->off_gamma);
+    h->keys_n = reinterpret_cast<unsigned long long*>(base + h->off_keys);
     TRY(dalloc(h, &h->xcomb, 1));
     CK(h, cudaMemsetAsync(h->xcomb, 0, sizeof(XComb), h->stream));
   } else {
@@ -857,7 +859,7 @@ rgdbek_status alloc_vectors(rgdbek_ctx* h) {
   TRY(dalloc(h, &h->ax, m));
   TRY(dalloc(h, &h->r, m));
   TRY(dalloc(h, &h->xi, m));
-  TRY(dalloc(h, &h->keys_n, n));
+  if (!h->peer) TRY(dalloc(h, &h->keys_n, n));          // peer ranks: in the arena
   TRY(dalloc(h, &h->keys_m, m));
   TRY(dalloc(h, &h->bpart, 4 * MAXBLK));
   TRY(dalloc(h, &h->hist, NBINS));
@@ -1037,9 +1039,16 @@ __global__ void k_gamma_combine(double* gamma, ShArgs x, const double* const* pg
 
 size_t sharded_smem(const rgdbek_ctx* h) { return h->p_dyn; }
 
+const void* sharded_kernel(bool dense, bool lazy) {
+  if (dense) return lazy ? (const void*)k_sharded<true, true> : (const void*)k_sharded<true, false>;
+  return lazy ? (const void*)k_sharded<false, true> : (const void*)k_sharded<false, false>;
+}
+
 rgdbek_status sharded_attr(rgdbek_ctx* h) {
-  const void* kf = h->dense ? (const void*)k_sharded<true> : (const void*)k_sharded<false>;
-  CK(h, cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sharded_smem(h)));
+  for (int lz = 0; lz < 2; ++lz)
+    CK(h, cudaFuncSetAttribute(sharded_kernel(h->dense, lz != 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sharded_smem(h)));
+  const void* kf = sharded_kernel(h->dense, h->lazyP != 0);
   int occ = 0;
   CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, PT, sharded_smem(h)));
   if (occ < 1) return set_err(h, RGDBEK_E_CUDA, "sharded kernel cannot be resident");
@@ -1067,6 +1076,7 @@ void sharded_peer(ShArgs& x, int r, const rgdbek_ctx* h, char* base) {
   x.px[r] = reinterpret_cast<double*>(base + h->off_x);
   x.pflags[r] = reinterpret_cast<XFlags*>(base + h->off_flags);
   x.ppub[r] = reinterpret_cast<XPub*>(base + h->off_pub);
+  x.pkeys[r] = reinterpret_cast<unsigned long long*>(base + h->off_keys);
 }
 
 const double* arena_gamma(const rgdbek_ctx* h, char* base) {
@@ -1084,7 +1094,7 @@ rgdbek_status run_loop(rgdbek_ctx* h, rgdbek_result* res) {
     CK(h, cudaMemcpyAsync(h->d_sa, &h->sh, sizeof(ShArgs), cudaMemcpyHostToDevice, h->stream));
     CK(h, cudaEventRecord(h->ev0, h->stream));
     void* args[] = {(void*)&h->d_pa, (void*)&h->d_sa};
-    const void* kf = h->dense ? (const void*)k_sharded<true> : (const void*)k_sharded<false>;
+    const void* kf = sharded_kernel(h->dense, h->lazyP != 0);
     CK(h, cudaLaunchCooperativeKernel(kf, dim3(h->pG, 1), dim3(PT), args, sharded_smem(h), h->stream));
     CK(h, cudaEventRecord(h->ev1, h->stream));
     CK(h, cudaMemcpyAsync(h->st_host, h->st, sizeof(Scal), cudaMemcpyDeviceToHost, h->stream));
@@ -1526,6 +1536,9 @@ rgdbek_status rgdbek_launch_kernel(rgdbek_handle h, int32_t kernel, int32_t reps
   if (kernel < 0 || kernel > 1 || reps < 0) return set_err(h, RGDBEK_E_ARG, "bad kernel id / reps");
   // never halt inside the timing loop
   k_call_begin<<<1, 1, 0, h->stream>>>(h->st, 1LL << 60, 1, 0.0, RGDBEK_STOP_NONE);
+  // pass T always computes both products (A^T z and A^T xi): the timing is the
+  // iteration's pass, not the first iteration's single product
+  k_set_pending<<<1, 1, 0, h->stream>>>(h->st);
   const double m = (double)h->m_loc, n = (double)h->n;
   double bytes;
   if (h->dense) {
@@ -1612,11 +1625,24 @@ rgdbek_status rgdbek_set_lazy(rgdbek_handle h, int32_t processes) {
   if (processes < 0 || processes > LZ_MAX)
     return set_err(h, RGDBEK_E_ARG, "processes must lie in [0, %d]", LZ_MAX);
   if (processes == 0) {                  // back to Algorithm 1
+    if (h->peer && (h->group || h->connected)) return set_err(h, RGDBEK_E_STATE, "set the algorithm before grouping / connecting");
     h->lazyP = 0;
     if (h->pG_base) h->pG = h->pG_base;
     return RGDBEK_OK;
   }
-  if (!h->dense || h->engine != 0 || h->dist || h->peer)
+  if (h->peer) {
+    // Algorithm 2 ACROSS the peer-sharded ranks: every rank is one process (processes = 1
+    // marks the rank; all ranks of a group must agree), dense or sparse A
+    if (processes != 1) return set_err(h, RGDBEK_E_ARG, "a peer-sharded rank is ONE process of Algorithm 2: use 1 (or 0)");
+    if (h->group || h->connected) return set_err(h, RGDBEK_E_STATE, "set the algorithm before grouping / connecting");
+    if (h->mode != 0 || h->pargs.greedy)
+      return set_err(h, RGDBEK_E_STATE, "Algorithm 2 needs the pseudoinverse-free update and random selection");
+    if (!h->pargs.lz_g) TRY(dalloc(h, &h->pargs.lz_g, h->n));
+    h->pargs.lz_kr[0] = std::max(1LL, (long long)std::floor(h->eta * (double)h->m_loc + 0.5));
+    h->lazyP = 1;
+    return RGDBEK_OK;
+  }
+  if (!h->dense || h->engine != 0 || h->dist)
     return set_err(h, RGDBEK_E_STATE, "Algorithm 2 runs on the single-GPU persistent engine, dense A");
   if (h->mode != 0 || h->pargs.greedy)
     return set_err(h, RGDBEK_E_STATE, "Algorithm 2 needs the pseudoinverse-free update and random selection");
@@ -1776,7 +1802,7 @@ rgdbek_status rgdbek_peer_window(rgdbek_handle h, int64_t* out4) {
 }  // extern "C"
 
 struct rgdbek_group_s {
-  int R = 0, G = 0, dense = 0;
+  int R = 0, G = 0, dense = 0, lazy = 0;
   rgdbek_ctx* h[MAXR] = {};
   PArgs* d_pa = nullptr;
   ShArgs* d_sa = nullptr;
@@ -1809,7 +1835,7 @@ rgdbek_status group_run(rgdbek_group_s* g, rgdbek_result* res) {
   }
   CK(h0, cudaEventRecord(g->ev0, st));
   void* args[] = {(void*)&g->d_pa, (void*)&g->d_sa};
-  const void* kf = g->dense ? (const void*)k_sharded<true> : (const void*)k_sharded<false>;
+  const void* kf = sharded_kernel(g->dense, g->lazy);
   CK(h0, cudaLaunchCooperativeKernel(kf, dim3(g->G, g->R), dim3(PT), args, sharded_smem(h0), st));
   CK(h0, cudaEventRecord(g->ev1, st));
   for (int r = 0; r < g->R; ++r)
@@ -1847,9 +1873,11 @@ rgdbek_status rgdbek_group_create(rgdbek_group* out, const rgdbek_handle* handle
       return group_fail(g, RGDBEK_E_STATE, "group ranks must be created with a partial row range "
                                             "and no NCCL communicator");
     if (h->group || h->connected) return group_fail(g, RGDBEK_E_STATE, "a handle is already grouped / connected");
-    if (h->mode != 0 || h->pargs.greedy || h->lazyP)
-      return group_fail(g, RGDBEK_E_STATE, "the sharded engine runs Algorithm 1 (pseudoinverse-free, random selection)");
+    if (h->mode != 0 || h->pargs.greedy)
+      return group_fail(g, RGDBEK_E_STATE, "the sharded engine runs the pseudoinverse-free update with random selection");
     const rgdbek_ctx* h0 = handles[0];
+    if ((h->lazyP != 0) != (h0->lazyP != 0))
+      return group_fail(g, RGDBEK_E_STATE, "all ranks must run the same algorithm (rgdbek_set_lazy)");
     if (h->device != h0->device || h->n != h0->n || h->m != h0->m || h->dense != h0->dense)
       return group_fail(g, RGDBEK_E_DIM, "group ranks must share device, m, n and storage kind");
     const long long expect = r == 0 ? 0 : handles[r - 1]->row0 + handles[r - 1]->m_loc;
@@ -1858,6 +1886,7 @@ rgdbek_status rgdbek_group_create(rgdbek_group* out, const rgdbek_handle* handle
   }
   rgdbek_ctx* h0 = g->h[0];
   g->dense = h0->dense ? 1 : 0;
+  g->lazy = h0->lazyP ? 1 : 0;
   if (cudaSetDevice(h0->device) != cudaSuccess) return group_fail(g, RGDBEK_E_CUDA, "cudaSetDevice");
   for (int r = 0; r < nranks; ++r)
     if (cudaStreamSynchronize(g->h[r]->stream) != cudaSuccess) return group_fail(g, RGDBEK_E_CUDA, "stream sync");
@@ -1865,7 +1894,7 @@ rgdbek_status rgdbek_group_create(rgdbek_group* out, const rgdbek_handle* handle
   if (sharded_attr(h0) != RGDBEK_OK) return group_fail(g, RGDBEK_E_CUDA, h0->err.c_str());
   int nsm = 148, occ = 1;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h0->device);
-  const void* kf = g->dense ? (const void*)k_sharded<true> : (const void*)k_sharded<false>;
+  const void* kf = sharded_kernel(g->dense, g->lazy);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, PT, sharded_smem(h0));
   int G = (nsm * std::max(occ, 1)) / nranks;
   for (int r = 0; r < nranks; ++r) G = std::min(G, g->h[r]->pG);
@@ -1968,8 +1997,8 @@ rgdbek_status rgdbek_peer_connect(rgdbek_handle h, int32_t nranks, int32_t rank,
   if (h->group || h->connected) return set_err(h, RGDBEK_E_STATE, "already grouped / connected");
   if (nranks < 1 || nranks > MAXR || rank < 0 || rank >= nranks || !handles || !windows)
     return set_err(h, RGDBEK_E_ARG, "rgdbek_peer_connect: bad arguments");
-  if (h->mode != 0 || h->pargs.greedy || h->lazyP)
-    return set_err(h, RGDBEK_E_STATE, "the sharded engine runs Algorithm 1 (pseudoinverse-free, random selection)");
+  if (h->mode != 0 || h->pargs.greedy)
+    return set_err(h, RGDBEK_E_STATE, "the sharded engine runs the pseudoinverse-free update with random selection");
   std::vector<long long> win(2 * nranks), ob(nranks + 1);
   for (int i = 0; i < 2 * nranks; ++i) win[i] = windows[i];
   if (win[2 * rank] != h->wlo || win[2 * rank + 1] != h->whi)

@@ -54,6 +54,7 @@ struct __align__(16) XPub {           // one rank's contribution to one barrier
 
 struct __align__(16) XComb {          // the rank-local sum over ranks (read by all CTAs)
   double scal[XSLOTS];
+  double rs[XSLOTS][MAXR];            // the published scalars rank by rank (Algorithm 2)
   unsigned long long acc[2];
   unsigned long long prefix;          // level-3 bucket prefix and count below it
   long long below;
@@ -74,6 +75,7 @@ struct ShArgs {
   double* pv[MAXR];                   // peers' v
   double* pzeta[MAXR];                // peers' zeta (authoritative on their owned columns)
   double* px[MAXR];                   // peers' x
+  unsigned long long* pkeys[MAXR];    // peers' column keys (Algorithm 2: U on the halo)
   XFlags* pflags[MAXR];               // peers' flag blocks (this rank writes arrive[.][rank])
   XPub* ppub[MAXR];                   // peers' publish blocks [2] (parity of the barrier)
   XComb* comb;                        // this rank's combined block
@@ -199,7 +201,11 @@ __device__ void xsync(const PArgs& a, const ShArgs& x, unsigned int& bgen, unsig
   XComb* cb = x.comb;
   if (q.nslot != 0 && threadIdx.x < (q.nslot == -1 ? 1 : q.nslot)) {
     double t = 0.0;
-    for (int r = 0; r < x.R; ++r) t += __ldcv(&x.ppub[r][par].scal[threadIdx.x]);
+    for (int r = 0; r < x.R; ++r) {
+      const double v = __ldcv(&x.ppub[r][par].scal[threadIdx.x]);
+      cb->rs[threadIdx.x][r] = v;
+      t += v;
+    }
     cb->scal[threadIdx.x] = t;
   }
   if (q.acc && threadIdx.x < 2) {
@@ -384,10 +390,37 @@ __device__ void x_select(PSel* ps, const unsigned long long* __restrict__ keys, 
   x_rank_survivors(ps, x.comb);
 }
 
+// Rank-local exact selection (Algorithm 2's own rows): the single-GPU radix
+// levels over this rank's keys, separated by the rank's grid barrier.  The histogram
+// levels and the candidate count are zeroed by x_zero_local before their next use.
+__device__ void x_select_local(PSel* ps, const unsigned long long* __restrict__ keys, long long N,
+                               long long idx_base, long long kblock, unsigned int* gh, Cand* cand,
+                               unsigned int* ncand, unsigned int* h, const ShArgs& x,
+                               unsigned int& bgen, unsigned int* sh_u, long long* sh_l) {
+  grid_sync(x.bar, bgen);                          // the rank's level-1 histogram is complete
+  p_sel_level1(ps, gh, N, kblock, sh_u, sh_l);
+  if (ps->mode != SEL_PENDING) return;
+  p_sel_scan<2>(ps, keys, N, idx_base, gh + NBINS, cand, ncand, h);
+  grid_sync(x.bar, bgen);
+  p_sel_level2(ps, gh + NBINS, sh_u, sh_l);
+  p_sel_scan<3>(ps, keys, N, idx_base, gh + 2 * NBINS, cand, ncand, h);
+  grid_sync(x.bar, bgen);
+  p_sel_level3(ps, gh + 2 * NBINS, cand, ncand, keys, N, idx_base, h, sh_u, sh_l);
+}
+
+__device__ void x_zero_local(unsigned int* gh, unsigned int* ncand) {
+  for (int i = blockIdx.x * PT + threadIdx.x; i < 3 * NBINS; i += gridDim.x * PT) gh[i] = 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ncand = 0u;
+}
+
 // ---------------------------------------------------------------------------
-// The sharded persistent kernel (Algorithm 1, pseudoinverse-free, random selection).
+// The sharded persistent kernel: Algorithm 1 (LAZY = false) or the paper's parallel
+// Algorithm 2 over the R ranks as its processes (LAZY = true; reading R28: the global U
+// from A^T z, local first-Krylov z-steps and own-row samples J^(p) of round(eta d_p) rows,
+// the lazily averaged x += (1/R) sum_p (X_p / V_p) (A^(p))^T xi_p).
+// Pseudoinverse-free update, random selection.
 // ---------------------------------------------------------------------------
-template <bool DENSE>
+template <bool DENSE, bool LAZY>
 __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
                                                    const ShArgs* __restrict__ sa) {
   __shared__ __align__(16) unsigned int h[NBINS];
@@ -398,8 +431,10 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
   __shared__ PSel ps;
   __shared__ PArgs a;
   __shared__ ShArgs x;
+  __shared__ double lzX[MAXR], lzV[MAXR];        // Algorithm 2: every rank's X_p, V_p
   extern __shared__ __align__(16) double dyn[];
   if (threadIdx.x == 0) { a = pa[blockIdx.y]; x = sa[blockIdx.y]; }
+  if (threadIdx.x < MAXR) { lzX[threadIdx.x] = 0.0; lzV[threadIdx.x] = 0.0; }
   __syncthreads();
   TileRing tring{tbar + (threadIdx.x / TG) * TRING, 0u};
   if (!DENSE) tile_rings_init(tbar);
@@ -414,7 +449,7 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
   const int stop_mode = st->stop_mode, has_ref = st->has_ref;
   const unsigned long long seed = st->seed;
   const double xsnorm2 = st->xsnorm2;
-  const long long kc = st->kc, kr = st->kr;
+  const long long kc = st->kc, kr = LAZY ? a.lz_kr[0] : st->kr;
   int pending = st->pending;
   double X = st->X;
   long long kp_prev = st->kp_prev, kpp_prev = st->kpp_prev;
@@ -425,6 +460,7 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
   unsigned int* hm = a.hist + 3 * NBINS;
   Cand* cn = a.cand;
   Cand* cm = a.cand + CAND_CAP;
+  double* sown = LAZY ? a.lz_g : a.s;            // the owned columns' s = A^T z
   unsigned int bgen = 0, xg = st->xgen;
   if (threadIdx.x == 0) bgen = ld_acquire_u32(&x.bar->gen);
   const XComb* cb = x.comb;
@@ -496,9 +532,10 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
       xsync(a, x, bgen, xg, q, sh_u, sh_l);
       if (pending) {
         X = cb->scal[0];
+        if (LAZY && threadIdx.x < x.R) lzX[threadIdx.x] = cb->rs[0][threadIdx.x];
         const long long kppf = (long long)cb->acc[0];
         if (lead) {
-          if (kppf != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 2;
+          if (!LAZY && kppf != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 2;
           if (TraceRec* t = trace_at(tr, st, k - 1)) { t->kpp = kppf; t->hash_j = cb->acc[1]; t->X = X; }
         }
         kpp_prev = kppf;
@@ -515,24 +552,35 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
       XReq q = xreq();
       xsync(a, x, bgen, xg, q, sh_u, sh_l);
     }
+    if constexpr (LAZY) x_zero_local(hm, a.ncand + 1);   // the rank's row selection is read
 
     // ===== P2: owned columns: s, v summed over the ranks whose window holds them;
     //           column keys, level-1 histogram, V partial =====
     for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
     __syncthreads();
     double Vp = 0.0;
+    if constexpr (LAZY) {
+      // V_p = ||(A^(p))^T xi_p||^2 over this rank's window (its own partial)
+      if (pending)
+        for (long long j = x.wlo + (long long)blockIdx.x * PT + threadIdx.x; j < x.whi; j += (long long)G * PT) {
+          const double vj = a.v[j];
+          Vp += vj * vj;
+        }
+    }
     for (long long jl = (long long)blockIdx.x * PT + threadIdx.x; jl < nown; jl += (long long)G * PT) {
       const long long j = own0 + jl;
       double sj = 0.0, vj = 0.0;
       for (int r = 0; r < x.R; ++r) {
         if (j >= x.plo[r] && j < x.phi[r]) {
-          sj += ld_weak(x.ps[r] + j);
-          if (pending) vj += ld_weak(x.pv[r] + j);
+          sj += __ldcv(x.ps[r] + j);
+          if (!LAZY && pending) vj += __ldcv(x.pv[r] + j);
         }
       }
-      a.s[j] = sj;
-      a.v[j] = vj;
-      if (pending) Vp += vj * vj;
+      sown[j] = sj;
+      if constexpr (!LAZY) {
+        a.v[j] = vj;
+        if (pending) Vp += vj * vj;
+      }
       const double gm = a.gamma[j];
       const double eps = gm > 0.0 ? __ddiv_rn(__dmul_rn(sj, sj), gm) : 0.0;
       const unsigned long long key = sel_key(eps, (unsigned long long)j, k, 0u, seed, 0);
@@ -551,7 +599,9 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
       q.nslot = 1; q.slot[0] = SL_V;
       xsync(a, x, bgen, xg, q, sh_u, sh_l);
       V = cb->scal[0];
+      if (LAZY && threadIdx.x < x.R) lzV[threadIdx.x] = cb->rs[0][threadIdx.x];
     }
+    __syncthreads();
     const int do_x = pending && kpp_prev > 0 && V > 0.0;
     const double alpha_x = do_x ? __ddiv_rn(X, V) : 0.0;
     if (lead && pending) {
@@ -560,19 +610,31 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
     // ===== P3-P5: the global column selection U =====
     x_select(&ps, a.keys_n + own0, nown, own0, n, kc, hn, cn, a.ncand, h, a, x, bgen, xg, sh_u, sh_l);
     if (lead && ps.slow) st->selstat[1] += 1;
-    // zeta, Z, |U|, hash on owned columns; x_k = x_{k-1} + alpha_x v; ||x - x*||^2
+    // |U|, hash and Z on owned columns (Algorithm 1: zeta = s on U); x_k; ||x - x*||^2
     {
       double Zp = 0.0, Rp = 0.0;
       long long cnt = 0;
       unsigned long long hs = 0ull;
       for (long long jl = (long long)blockIdx.x * PT + threadIdx.x; jl < nown; jl += (long long)G * PT) {
         const long long j = own0 + jl;
-        const double sj = a.s[j];
+        const double sj = sown[j];
         const bool sel = p_selected(&ps, a.keys_n[j], j);
-        a.zeta[j] = sel ? sj : 0.0;
+        if (!LAZY) a.zeta[j] = sel ? sj : 0.0;
         if (sel) { Zp += sj * sj; cnt += 1; hs += splitmix64((unsigned long long)j); }
         double xj = a.x[j];
-        if (do_x) { xj = __dadd_rn(xj, __dmul_rn(alpha_x, a.v[j])); a.x[j] = xj; }
+        if constexpr (LAZY) {
+          // x_k = x_{k-1} + (1/R) sum_p (X_p / V_p) v_p, v_p over p's window
+          if (pending) {
+            double t = 0.0;
+            for (int r = 0; r < x.R; ++r)
+              if (lzX[r] > 0.0 && lzV[r] > 0.0 && j >= x.plo[r] && j < x.phi[r])
+                t = __dadd_rn(t, __dmul_rn(__ddiv_rn(lzX[r], lzV[r]), __ldcv(x.pv[r] + j)));
+            xj = __dadd_rn(xj, __ddiv_rn(t, (double)x.R));
+            a.x[j] = xj;
+          }
+        } else {
+          if (do_x) { xj = __dadd_rn(xj, __dmul_rn(alpha_x, a.v[j])); a.x[j] = xj; }
+        }
         if (has_ref) { const double d = xj - a.xstar[j]; Rp += d * d; }
       }
       if (a.capU)
@@ -601,19 +663,39 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
       kp = (long long)cb->acc[0];
       if (lead) {
         if (kp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 1;
-        if (TraceRec* t = trace_at(tr, st, k)) { t->k = k; t->kp = kp; t->hash_u = cb->acc[1]; t->Z = Z; }
+        if (TraceRec* t = trace_at(tr, st, k)) { t->k = k; t->kp = kp; t->hash_u = cb->acc[1]; if (!LAZY) t->Z = Z; }
       }
     }
-    // ===== halo: zeta, x of the window's columns owned by other ranks =====
-    for (int r = 0; r < x.R; ++r) {
-      if (r == x.rank) continue;
-      const long long lo = max(x.wlo, x.ownb[r]), hi = min(x.whi, x.ownb[r + 1]);
-      for (long long j = lo + (long long)blockIdx.x * PT + threadIdx.x; j < hi; j += (long long)G * PT) {
-        a.zeta[j] = ld_weak(x.pzeta[r] + j);
-        a.x[j] = ld_weak(x.px[r] + j);
+    // ===== halo: the window's columns owned by other ranks =====
+    double Zl = 0.0;                               // Algorithm 2: this rank's Z_p partial
+    if constexpr (LAZY) {
+      // zeta_p = (A^(p))^T z^(p) on U over the window; U on a halo column is
+      // decided from its owner's key
+      for (long long j = x.wlo + (long long)blockIdx.x * PT + threadIdx.x; j < x.whi; j += (long long)G * PT) {
+        int o = x.rank;
+        if (j < own0 || j >= x.own1)
+          for (int r = 0; r < x.R; ++r) if (j >= x.ownb[r] && j < x.ownb[r + 1]) o = r;
+        const unsigned long long key = o == x.rank ? a.keys_n[j] : __ldcv(x.pkeys[o] + j);
+        if (o != x.rank) a.x[j] = __ldcv(x.px[o] + j);
+        const double gj = a.s[j];
+        const bool sel = p_selected(&ps, key, j);
+        a.zeta[j] = sel ? gj : 0.0;
+        if (sel) Zl += gj * gj;
+      }
+      const double zb = pblock_sum(Zl, sh);
+      if (threadIdx.x == 0) bp[SL_MAXN * G + blockIdx.x] = zb;
+    } else {
+      for (int r = 0; r < x.R; ++r) {
+        if (r == x.rank) continue;
+        const long long lo = max(x.wlo, x.ownb[r]), hi = min(x.whi, x.ownb[r + 1]);
+        for (long long j = lo + (long long)blockIdx.x * PT + threadIdx.x; j < hi; j += (long long)G * PT) {
+          a.zeta[j] = __ldcv(x.pzeta[r] + j);
+          a.x[j] = __ldcv(x.px[r] + j);
+        }
       }
     }
     grid_sync(x.bar, bgen);
+    const double Zr = LAZY ? slot_sum(bp, SL_MAXN, sh) : Z;
 
     // ===== P6: pass N over the rank's rows (w = A zeta, A x_k), W / ||b - A x||^2 =====
     {
@@ -631,13 +713,15 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
       const double yb = pblock_sum(Yp, sh);
       if (threadIdx.x == 0) { bp[SL_W * G + blockIdx.x] = wb; bp[SL_Y * G + blockIdx.x] = yb; }
     }
-    double W, Y;
+    double W, Y, Wr;
     {
       XReq q = xreq();
-      q.nslot = 2; q.slot[0] = SL_W; q.slot[1] = SL_Y;
+      q.nslot = LAZY ? 3 : 2; q.slot[0] = SL_W; q.slot[1] = SL_Y; q.slot[2] = SL_MAXN;
       xsync(a, x, bgen, xg, q, sh_u, sh_l);
       W = cb->scal[0];
       Y = cb->scal[1];
+      Wr = LAZY ? cb->rs[0][x.rank] : W;
+      if (LAZY) Z = cb->scal[2];                 // sum over ranks of Z_p (trace)
     }
     // ===== P8: stop test on x_k; z_{k+1}, r, row keys, level-1 histogram =====
     {
@@ -651,7 +735,7 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
       }
       if (!halt && (k > k_begin || k_end == k_begin) && k >= k_end) { halt = 1; outcome = RGDBEK_MAX_ITER; }
       if (lead) {
-        if (TraceRec* t = trace_at(tr, st, k)) t->W = W;
+        if (TraceRec* t = trace_at(tr, st, k)) { t->W = W; if (LAZY) t->Z = Z; }
         if (k >= 1) { if (TraceRec* t = trace_at(tr, st, k - 1)) t->rse = rse; }
       }
       if (halt) {
@@ -670,8 +754,8 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
     for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
     __syncthreads();
     {
-      const int doz = kp > 0 && W > 0.0;
-      const double az = doz ? __ddiv_rn(Z, W) : 0.0;
+      const int doz = kp > 0 && Wr > 0.0;
+      const double az = doz ? __ddiv_rn(Zr, Wr) : 0.0;
       for (int i = blockIdx.x * PT + threadIdx.x; i < m_loc; i += G * PT) {
         double zi = a.z[i];
         if (doz) { zi = __dsub_rn(zi, __dmul_rn(az, a.w[i])); a.z[i] = zi; }
@@ -686,9 +770,13 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
     }
     __syncthreads();
     flush_hist<PT>(h, hm, NBINS);
-    // ===== P9-P11: the global row selection J =====
-    x_select(&ps, a.keys_m, m_loc, a.row0, m_glob, kr, hm, cm, a.ncand + 1, h, a, x, bgen, xg,
-             sh_u, sh_l);
+    // ===== P9-P11: the row selection J (Algorithm 2: this rank's own rows) =====
+    if constexpr (LAZY) {
+      x_select_local(&ps, a.keys_m, m_loc, a.row0, kr, hm, cm, a.ncand + 1, h, x, bgen, sh_u, sh_l);
+    } else {
+      x_select(&ps, a.keys_m, m_loc, a.row0, m_glob, kr, hm, cm, a.ncand + 1, h, a, x, bgen, xg,
+               sh_u, sh_l);
+    }
     if (lead && ps.slow) st->selstat[1] += 1;
     if constexpr (!DENSE) {
       // xi = r on J, X, |J|, hash (dense: formed in the next pass T)
@@ -718,9 +806,10 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
       q.acc = a.acc + 2;
       xsync(a, x, bgen, xg, q, sh_u, sh_l);
       X = cb->scal[0];
+      if (LAZY && threadIdx.x < x.R) lzX[threadIdx.x] = cb->rs[0][threadIdx.x];
       const long long kpp = (long long)cb->acc[0];
       if (lead) {
-        if (kpp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 2;
+        if (!LAZY && kpp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 2;
         if (TraceRec* t = trace_at(tr, st, k)) { t->kpp = kpp; t->hash_j = cb->acc[1]; t->X = X; }
       }
       kpp_prev = kpp;

@@ -160,3 +160,46 @@ def test_group_argument_checks():
             g.close()
     with pytest.raises(RgdbekError):
         a.set_mode("exact")
+
+
+@pytest.mark.parametrize("R", [2, 4])
+@pytest.mark.parametrize("name", ["C2s", "C5t", "C3s"])
+def test_algorithm_2_across_ranks(name, R):
+    """The paper's parallel Algorithm 2 (reading R28) with the R ranks as its
+    processes, dense and sparse A: the global U from A^T z, each rank's first-Krylov
+    z-step and own-row sample J^(p) of round(eta d_p) rows, and the lazily averaged
+    x-update — against oracle/lazy.py on the same nnz-balanced row blocks."""
+    from oracle.lazy import LazyOracle
+    from paper_2509_19267_b200 import Solver, ShardGroup
+    from paper_2509_19267_b200.dist import partition_rows, shard_csr
+    from workloads import by_name
+    w = by_name(name)
+    m, n = w.shape
+    parts = partition_rows(m if w.dense else w.A.indptr, R)
+    ss = []
+    for (r0, r1) in parts:
+        if w.dense:
+            s = Solver(w.A[r0:r1], w.b[r0:r1], eta=w.eta, m=m, row_range=(r0, r1))
+        else:
+            rp, ci, val = shard_csr(*w.csr_arrays(), r0, r1)
+            s = Solver.from_csr(m, n, rp, ci, val, w.b[r0:r1], eta=w.eta, row_range=(r0, r1))
+        s.set_lazy(1)
+        s.set_capture(True)
+        ss.append(s)
+    g = ShardGroup(ss)
+    o = LazyOracle(w.A, w.b, w.eta, bounds=parts)
+    g.reset(2)
+    bn = np.linalg.norm(w.b)
+    for k in range(20):
+        rec = o.iterate(2, keep_blocks=True)
+        g.step(1)
+        t = ss[0].trace()[-1]
+        assert (t["kp"], t["hash_u"], t["kpp"], t["hash_j"]) == (rec.kp, rec.hash_u, rec.kpp, rec.hash_j), k
+        for f in ("Z", "W", "X", "V"):
+            assert abs(t[f] - getattr(rec, f)) <= 1e-9 * max(abs(getattr(rec, f)), 1e-300), (k, f)
+        U, J = _lists(ss)
+        assert np.array_equal(U, rec.U) and np.array_equal(J, rec.J), k
+        assert np.linalg.norm(ss[0].x() - o.x) <= 1e-10 * max(np.linalg.norm(o.x), 1e-300), k
+        z = np.concatenate([s.z() for s in ss])
+        assert np.linalg.norm(z - o.z) <= 1e-10 * bn, k
+    _close(ss, g)

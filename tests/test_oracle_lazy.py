@@ -88,3 +88,16 @@ def test_two_processes_converge_on_this_consistent_system():
     o = LazyOracle(A, b, 0.5, parts=2)
     out, iters, rse, rel = o.solve(1e-8, 20000, 0, stop=STOP_REL_ERR, xstar=xs)
     assert out == OUTCOME_CONVERGED and rel <= 1e-8
+
+
+def test_explicit_bounds_equal_the_default_partition():
+    from workloads import dense_gaussian
+    w = dense_gaussian(90, 20, seed=4)
+    a = LazyOracle(w.A, w.b, 0.5, parts=3)
+    b = LazyOracle(w.A, w.b, 0.5, bounds=[(0, 30), (30, 60), (60, 90)])
+    for _ in range(5):
+        ra, rb = a.iterate(2), b.iterate(2)
+        assert (ra.hash_u, ra.hash_j) == (rb.hash_u, rb.hash_j)
+    assert np.array_equal(a.x, b.x) and np.array_equal(a.z, b.z)
+    with pytest.raises(ValueError):
+        LazyOracle(w.A, w.b, 0.5, bounds=[(0, 30), (31, 90)])

@@ -295,6 +295,9 @@ CONFIGS = {
     # C5's matrix with a consistent b (no null-space noise: skips the 1.7M block SVDs);
     # same A, same bytes per iteration — used for ncu captures of the C5 kernel
     "C5c": lambda: _throughput_only(popmodel(50_000_000, 5_000_000, seed=0, noise_frac=0.0)),
+    # a tenth of C5 (same structure, 1e8 nnz, consistent b): quick to generate, large
+    # enough to be bandwidth-bound (kernel experiments, tools/ab_pass.py)
+    "C5m": lambda: _throughput_only(popmodel(5_000_000, 500_000, seed=0, noise_frac=0.0)),
     # small twins used by parity tests
     "C2s": lambda: dense_gaussian(2000, 500, seed=0),
     "C2si": lambda: dense_gaussian(2000, 500, seed=0, noise=0.1),
