@@ -304,6 +304,29 @@ rgdbek_status rgdbek_peer_export(rgdbek_handle h, void* out_handle);
 rgdbek_status rgdbek_peer_connect(rgdbek_handle h, int32_t nranks, int32_t rank,
                                   const void* handles, const int64_t* windows);
 
+/* ---------------------------------------------------------------------------------------
+ * Several right-hand sides sharing A (the paper's 3-channel deblurring
+ * solves A x_i = b_i with one blur operator).  nrhs <= 4 independent Algorithm-1
+ * solves (reading R29): right-hand side q has its own z, x, blocks and Philox
+ * stream with seed + q, so it follows exactly the single-RHS solve of (A, b_q, seed + q);
+ * every pass over A serves all of them.  b_all holds nrhs vectors of m values, RHS-major
+ * (b_all[q * m + i]).  Sparse A, one GPU, all rows; pseudoinverse-free update and random
+ * selection (RGDBEK_E_STATE otherwise).  rgdbek_step / rgdbek_solve run all right-hand
+ * sides together; solve stops when every right-hand side meets the stop test (or stalls),
+ * or at max_iter.  The rgdbek_result and the plain getters describe right-hand side 0;
+ * the *_rhs calls address right-hand side `rhs` (RGDBEK_E_ARG outside [0, nrhs)).
+ * STOP_REL_ERR needs rgdbek_set_reference_rhs for every right-hand side. */
+rgdbek_status rgdbek_create_csr_multi(rgdbek_handle* out, int64_t m, int64_t n, int64_t nnz,
+                                      const int64_t* row_ptr, const int32_t* col_idx,
+                                      const double* val, const double* b_all, int32_t nrhs,
+                                      const rgdbek_options* opts);
+int32_t       rgdbek_rhs_count(rgdbek_handle h);
+rgdbek_status rgdbek_get_x_rhs(rgdbek_handle h, int32_t rhs, double* out_n);
+rgdbek_status rgdbek_get_z_rhs(rgdbek_handle h, int32_t rhs, double* out_m);
+rgdbek_status rgdbek_set_reference_rhs(rgdbek_handle h, int32_t rhs, const double* xstar);
+rgdbek_status rgdbek_get_trace_rhs(rgdbek_handle h, int32_t rhs, rgdbek_trace_record* out,
+                                   int64_t max_records, int64_t* n_out);
+
 /* NCCL bootstrap helpers (rank 0 makes the id; it is broadcast by the caller). */
 rgdbek_status rgdbek_nccl_unique_id(void* out_128_bytes);
 rgdbek_status rgdbek_nccl_comm_init(void** comm_out, int32_t nranks, int32_t rank,

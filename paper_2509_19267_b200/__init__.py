@@ -88,6 +88,51 @@ class Solver:
         return self
 
     @classmethod
+    def from_scipy_multi(cls, A, B, eta=0.5, stop="rse", device=0, stream=None, trace_capacity=4096):
+        """Several right-hand sides sharing sparse A (rgdbek_create_csr_multi): B is
+        (nrhs, m); right-hand side q follows the single-RHS solve with seed + q."""
+        A = A.tocsr(copy=True)
+        A.sort_indices()
+        B = np.ascontiguousarray(B, dtype=np.float64)
+        if B.ndim != 2 or B.shape[1] != A.shape[0]:
+            raise ValueError("B must be (nrhs, m)")
+        self = cls.__new__(cls)
+        Solver.__init__(self, eta=eta, stop=stop, device=device, stream=stream,
+                        trace_capacity=trace_capacity, _handle=0, _shape=(A.shape[0], A.shape[1], 0))
+        self._h = None
+        prp, k1 = _ptr(A.indptr.astype(np.int64), np.int64)
+        pci, k2 = _ptr(A.indices.astype(np.int32), np.int32)
+        pv, k3 = _ptr(A.data.astype(np.float64), np.float64)
+        pb, k4 = _ptr(B, np.float64)
+        self._h = N.rgdbek_create_csr_multi(A.shape[0], A.shape[1], A.nnz, prp, pci, pv, pb,
+                                            B.shape[0], self._opts)
+        self.m, self.n, self.m_local = A.shape[0], A.shape[1], A.shape[0]
+        return self
+
+    @property
+    def nrhs(self):
+        return N.rgdbek_rhs_count(self._h)
+
+    def x_rhs(self, rhs):
+        out = np.empty(self.n)
+        N.rgdbek_get_x_rhs(self._h, int(rhs), _out_ptr(out, self.n))
+        return out
+
+    def z_rhs(self, rhs):
+        out = np.empty(self.m_local)
+        N.rgdbek_get_z_rhs(self._h, int(rhs), _out_ptr(out, self.m_local))
+        return out
+
+    def set_reference_rhs(self, rhs, xstar):
+        p, keep = _ptr(xstar, np.float64)
+        N.rgdbek_set_reference_rhs(self._h, int(rhs), p)
+
+    def trace_rhs(self, rhs, max_records=1 << 20):
+        recs = N.rgdbek_get_trace_rhs(self._h, int(rhs), max_records)
+        return [dict(k=r.k, kp=r.kp, hash_u=r.hash_u, Z=r.Z, W=r.W, kpp=r.kpp, hash_j=r.hash_j,
+                     X=r.X, V=r.V, rse=r.rse) for r in recs]
+
+    @classmethod
     def from_scipy(cls, A, b, **kw):
         A = A.tocsr(copy=True)                       # never reorder the caller's matrix
         A.sort_indices()

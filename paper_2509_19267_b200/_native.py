@@ -26,7 +26,8 @@ EXPORTED = [
     "rgdbek_set_selection", "rgdbek_set_lazy", "rgdbek_set_capture", "rgdbek_selection_stats",
     "rgdbek_build_info", "rgdbek_plan_ownership", "rgdbek_peer_window", "rgdbek_group_create",
     "rgdbek_group_reset", "rgdbek_group_step", "rgdbek_group_solve", "rgdbek_group_destroy",
-    "rgdbek_peer_export", "rgdbek_peer_connect",
+    "rgdbek_peer_export", "rgdbek_peer_connect", "rgdbek_create_csr_multi", "rgdbek_rhs_count",
+    "rgdbek_get_x_rhs", "rgdbek_get_z_rhs", "rgdbek_set_reference_rhs", "rgdbek_get_trace_rhs",
     "rgdbek_nccl_unique_id", "rgdbek_nccl_comm_init", "rgdbek_nccl_comm_destroy",
     "rgdbek_last_error", "rgdbek_destroy",
 ]
@@ -115,6 +116,14 @@ def load(path=None):
                                          C.POINTER(rgdbek_result)]),
         "rgdbek_group_destroy": (None, [C.c_void_p]),
         "rgdbek_peer_export": (C.c_int, [H, P]),
+        "rgdbek_create_csr_multi": (C.c_int, [C.POINTER(H), C.c_int64, C.c_int64, C.c_int64, P, P, P,
+                                              P, C.c_int32, C.POINTER(rgdbek_options)]),
+        "rgdbek_rhs_count": (C.c_int32, [H]),
+        "rgdbek_get_x_rhs": (C.c_int, [H, C.c_int32, P]),
+        "rgdbek_get_z_rhs": (C.c_int, [H, C.c_int32, P]),
+        "rgdbek_set_reference_rhs": (C.c_int, [H, C.c_int32, P]),
+        "rgdbek_get_trace_rhs": (C.c_int, [H, C.c_int32, C.POINTER(rgdbek_trace_record), C.c_int64,
+                                           C.POINTER(C.c_int64)]),
         "rgdbek_peer_connect": (C.c_int, [H, C.c_int32, C.c_int32, P, C.POINTER(C.c_int64)]),
         "rgdbek_nccl_unique_id": (C.c_int, [P]),
         "rgdbek_nccl_comm_init": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, P,
@@ -162,6 +171,36 @@ def rgdbek_create_csr(m, n, nnz, row_ptr, col_idx, val, b_ptr, opts):
     check(load().rgdbek_create_csr(C.byref(h), m, n, nnz, row_ptr, col_idx, val, b_ptr,
                                    C.byref(opts)), None)
     return h
+
+
+def rgdbek_create_csr_multi(m, n, nnz, row_ptr, col_idx, val, b_all, nrhs, opts):
+    h = C.c_void_p()
+    check(load().rgdbek_create_csr_multi(C.byref(h), m, n, nnz, row_ptr, col_idx, val, b_all, nrhs,
+                                         C.byref(opts)), None)
+    return h
+
+
+def rgdbek_rhs_count(h):
+    return load().rgdbek_rhs_count(h)
+
+
+def rgdbek_get_x_rhs(h, rhs, out_ptr):
+    check(load().rgdbek_get_x_rhs(h, rhs, out_ptr), h)
+
+
+def rgdbek_get_z_rhs(h, rhs, out_ptr):
+    check(load().rgdbek_get_z_rhs(h, rhs, out_ptr), h)
+
+
+def rgdbek_set_reference_rhs(h, rhs, ptr):
+    check(load().rgdbek_set_reference_rhs(h, rhs, ptr), h)
+
+
+def rgdbek_get_trace_rhs(h, rhs, max_records):
+    buf = (rgdbek_trace_record * max(int(max_records), 1))()
+    cnt = C.c_int64()
+    check(load().rgdbek_get_trace_rhs(h, rhs, buf, max_records, C.byref(cnt)), h)
+    return [buf[i] for i in range(cnt.value)]
 
 
 def rgdbek_reset(h, seed):

@@ -615,6 +615,23 @@ __global__ void k_reset_vecs(double* x, int n, double* z, const double* b, int m
   for (long long j = t; j < n; j += str) x[j] = 0.0;
   for (long long i = t; i < m_loc; i += str) z[i] = b[i];
 }
+// multi-RHS reset: x = 0 ([n][nr]), z = b ([m][nr], interleaved)
+__global__ void k_reset_multi(double* x, long long nx, double* z, const double* b, long long nz) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long str = (long long)gridDim.x * blockDim.x;
+  for (long long j = t; j < nx; j += str) x[j] = 0.0;
+  for (long long i = t; i < nz; i += str) z[i] = b[i];
+}
+// [nr][len] <-> [len][nr]
+__global__ void k_interleave(const double* src, double* dst, long long len, int nr, int to_inter) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < len * nr;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / nr, q = e - i * nr;       // dst/src index e = i * nr + q
+    if (to_inter) dst[e] = src[q * len + i];
+    else dst[q * len + i] = src[e];
+  }
+}
+
 __global__ void k_reset_scal(Scal* st, unsigned long long seed, long long k) {
   st->k = k;
   st->k_begin = k;

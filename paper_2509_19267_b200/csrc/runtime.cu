@@ -21,6 +21,7 @@
 
 #include "exact.cuh"
 #include "sharded.cuh"
+#include "multi.cuh"
 
 using namespace rg;
 
@@ -134,6 +135,11 @@ struct rgdbek_ctx {
   void* ipc_open[MAXR] = {};            // peer arenas opened by cudaIpcOpenMemHandle
   PArgs* d_pa = nullptr;                // device copies for the sharded launch
   ShArgs* d_sa = nullptr;
+  // several right-hand sides sharing A (multi.cuh, rgdbek_create_csr_multi)
+  int nrhs = 1;
+  unsigned int ref_mask = 0;            // right-hand sides with a reference x*
+  MArgs margs{};
+  Scal* mst_host[MAXRHS] = {};          // pinned mirrors of the per-RHS scalars
   // errors
   int sticky = 0;
   std::string err;
@@ -716,6 +722,13 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
 
 rgdbek_status launch_persistent(rgdbek_ctx* h) {
   h->pargs.pt_rows = h->mode == 1 ? h->pt_rows_env : 0;
+  if (h->nrhs > 1) {
+    void* args[] = {(void*)&h->pargs, (void*)&h->margs};
+    const void* kf = h->nrhs == 2 ? (const void*)k_multi<2> : h->nrhs == 3 ? (const void*)k_multi<3>
+                                                                           : (const void*)k_multi<4>;
+    CK(h, cudaLaunchCooperativeKernel(kf, dim3(h->pG), dim3(PT), args, h->p_dyn, h->stream));
+    return RGDBEK_OK;
+  }
   if (h->mode == 1) {
     void* args[] = {(void*)&h->pargs, (void*)&h->eargs};
     const void* kx = h->dense ? (const void*)k_persistent_exact<true> : (const void*)k_persistent_exact<false>;
@@ -1188,6 +1201,7 @@ void rgdbek_destroy(rgdbek_handle h) {
     cudaCtxResetPersistingL2Cache();
   }
   for (int q = 0; q < MAXR; ++q) if (h->ipc_open[q]) cudaIpcCloseMemHandle(h->ipc_open[q]);
+  for (int q = 0; q < MAXRHS; ++q) if (h->mst_host[q]) cudaFreeHost(h->mst_host[q]);
   if (h->exec) cudaGraphExecDestroy(h->exec);
   if (h->graph) cudaGraphDestroy(h->graph);
   if (h->body_exec) cudaGraphExecDestroy(h->body_exec);
@@ -1367,6 +1381,14 @@ rgdbek_status rgdbek_create_csr(rgdbek_handle* out, int64_t m, int64_t n, int64_
 
 rgdbek_status rgdbek_reset(rgdbek_handle h, uint64_t seed) {
   TRY(ensure_usable(h));
+  if (h->nrhs > 1) {
+    for (int q = 0; q < h->nrhs; ++q) k_reset_scal<<<1, 1, 0, h->stream>>>(h->margs.st[q], seed, 0);
+    k_reset_multi<<<nblocks(std::max(h->n, h->m_loc) * h->nrhs, 256, 2048), 256, 0, h->stream>>>(
+        h->margs.x, h->n * h->nrhs, h->margs.z, h->margs.b, h->m_loc * h->nrhs);
+    CK(h, cudaGetLastError());
+    CK(h, cudaStreamSynchronize(h->stream));
+    return RGDBEK_OK;
+  }
   k_reset_scal<<<1, 1, 0, h->stream>>>(h->st, seed, 0);
   k_reset_vecs<<<nblocks(std::max(h->n, h->m_loc), 256, 1184), 256, 0, h->stream>>>(
       h->x, (int)h->n, h->z, h->b, (int)h->m_loc);
@@ -1385,6 +1407,7 @@ rgdbek_status rgdbek_set_stop(rgdbek_handle h, int32_t stop) {
 rgdbek_status rgdbek_set_reference(rgdbek_handle h, const double* xstar) {
   TRY(ensure_usable(h));
   if (!xstar) return set_err(h, RGDBEK_E_ARG, "NULL xstar");
+  if (h->nrhs > 1) return rgdbek_set_reference_rhs(h, 0, xstar);
   CK(h, cudaMemcpyAsync(h->xstar, xstar, h->n * sizeof(double), cudaMemcpyDefault, h->stream));
   std::vector<double> hx(h->n);
   CK(h, cudaMemcpyAsync(hx.data(), h->xstar, h->n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -1427,6 +1450,7 @@ rgdbek_status rgdbek_solve(rgdbek_handle h, double tol, int64_t max_iter, uint64
 rgdbek_status rgdbek_get_x(rgdbek_handle h, double* out) {
   TRY(ensure_usable(h));
   if (!out) return set_err(h, RGDBEK_E_ARG, "NULL out");
+  if (h->nrhs > 1) return rgdbek_get_x_rhs(h, 0, out);   // right-hand side 0
   if (h->peer && (h->group || h->connected)) {
     // x is authoritative on each rank's owned columns: gather them (peer reads)
     const ShArgs& x = h->sh;
@@ -1447,6 +1471,7 @@ rgdbek_status rgdbek_get_x(rgdbek_handle h, double* out) {
 rgdbek_status rgdbek_get_z(rgdbek_handle h, double* out) {
   TRY(ensure_usable(h));
   if (!out) return set_err(h, RGDBEK_E_ARG, "NULL out");
+  if (h->nrhs > 1) return rgdbek_get_z_rhs(h, 0, out);
   CK(h, cudaMemcpyAsync(out, h->z, h->m_loc * sizeof(double), cudaMemcpyDefault, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
   return RGDBEK_OK;
@@ -1519,6 +1544,7 @@ rgdbek_status rgdbek_get_trace(rgdbek_handle h, rgdbek_trace_record* out, int64_
 
 rgdbek_status rgdbek_set_state(rgdbek_handle h, const double* x, const double* z_local, int64_t k) {
   TRY(ensure_usable(h));
+  if (h->nrhs > 1) return set_err(h, RGDBEK_E_STATE, "set_state: single right-hand side");
   if (!x || !z_local || k < 0) return set_err(h, RGDBEK_E_ARG, "bad arguments");
   CK(h, cudaMemcpyAsync(h->x, x, h->n * sizeof(double), cudaMemcpyDefault, h->stream));
   CK(h, cudaMemcpyAsync(h->z, z_local, h->m_loc * sizeof(double), cudaMemcpyDefault, h->stream));
@@ -1581,6 +1607,8 @@ rgdbek_status rgdbek_phase_times(rgdbek_handle h, double* out_ns, int32_t max_ph
 
 rgdbek_status rgdbek_set_mode(rgdbek_handle h, int32_t mode, double inner_tol, int32_t inner_max) {
   TRY(ensure_usable(h));
+  if (mode != 0 && h->nrhs > 1)
+    return set_err(h, RGDBEK_E_STATE, "multiple right-hand sides run the pseudoinverse-free update");
   if (mode != 0 && h->peer)
     return set_err(h, RGDBEK_E_STATE, "the peer-sharded engine runs the pseudoinverse-free update");
   if (mode < 0 || mode > 1) return set_err(h, RGDBEK_E_ARG, "unknown update mode %d", mode);
@@ -1609,7 +1637,7 @@ rgdbek_status rgdbek_set_mode(rgdbek_handle h, int32_t mode, double inner_tol, i
 rgdbek_status rgdbek_set_selection(rgdbek_handle h, int32_t selection) {
   TRY(ensure_usable(h));
   if (selection < 0 || selection > 1) return set_err(h, RGDBEK_E_ARG, "unknown selection rule %d", selection);
-  if (selection == 1 && (h->engine != 0 || h->dist || h->peer))
+  if (selection == 1 && (h->engine != 0 || h->dist || h->peer || h->nrhs > 1))
     return set_err(h, RGDBEK_E_STATE, "greedy selection runs on the single-GPU persistent engine");
   if (selection == 1 && h->lazyP)
     return set_err(h, RGDBEK_E_STATE, "Algorithm 2 (set_lazy) samples its blocks (random selection only)");
@@ -1622,6 +1650,7 @@ rgdbek_status rgdbek_set_selection(rgdbek_handle h, int32_t selection) {
 // persistent kernel, so its row block is [floor(m p / P), floor(m (p+1) / P)).
 rgdbek_status rgdbek_set_lazy(rgdbek_handle h, int32_t processes) {
   TRY(ensure_usable(h));
+  if (processes != 0 && h->nrhs > 1) return set_err(h, RGDBEK_E_STATE, "Algorithm 2 is not combined with multiple right-hand sides");
   if (processes < 0 || processes > LZ_MAX)
     return set_err(h, RGDBEK_E_ARG, "processes must lie in [0, %d]", LZ_MAX);
   if (processes == 0) {                  // back to Algorithm 1
@@ -1688,6 +1717,7 @@ rgdbek_status rgdbek_set_lazy(rgdbek_handle h, int32_t processes) {
 
 rgdbek_status rgdbek_set_capture(rgdbek_handle h, int32_t enable) {
   TRY(ensure_usable(h));
+  if (enable && h->nrhs > 1) return set_err(h, RGDBEK_E_STATE, "block capture: single right-hand side (use the per-RHS traces)");
   if (enable) {
     if (!h->selmask_n) {
       TRY(dalloc(h, &h->selmask_n, 2 * h->n));
@@ -1777,6 +1807,198 @@ rgdbek_status rgdbek_nccl_comm_init(void** comm_out, int32_t nranks, int32_t ran
   if (!f || f(comm_out, nranks, id, rank) != 0) return set_err(nullptr, RGDBEK_E_NCCL, "ncclCommInitRank failed");
   return RGDBEK_OK;
 }
+
+}  // extern "C"
+
+// ===========================================================================
+// Several right-hand sides sharing A (multi.cuh)
+// ===========================================================================
+namespace {
+
+rgdbek_status setup_multi(rgdbek_ctx* h, const double* b_all, int nr) {
+  if (h->dense || h->engine != 0 || h->dist || h->peer)
+    return set_err(h, RGDBEK_E_STATE, "multiple right-hand sides run on the single-GPU persistent engine, sparse A");
+  const long long n = h->n, m = h->m_loc;
+  MArgs& ma = h->margs;
+  memset(&ma, 0, sizeof ma);
+  ma.nr = nr;
+  TRY(dalloc(h, &ma.x, n * nr));
+  TRY(dalloc(h, &ma.s, n * nr));
+  TRY(dalloc(h, &ma.v, n * nr));
+  TRY(dalloc(h, &ma.zeta, n * nr));
+  TRY(dalloc(h, &ma.xstar, n * nr));
+  TRY(dalloc(h, &ma.z, m * nr));
+  TRY(dalloc(h, &ma.w, m * nr));
+  TRY(dalloc(h, &ma.ax, m * nr));
+  TRY(dalloc(h, &ma.r, m * nr));
+  TRY(dalloc(h, &ma.xi, m * nr));
+  TRY(dalloc(h, &ma.b, m * nr));
+  CK(h, cudaMemsetAsync(ma.xi, 0, m * nr * sizeof(double), h->stream));
+  CK(h, cudaMemsetAsync(ma.v, 0, n * nr * sizeof(double), h->stream));
+  CK(h, cudaMemsetAsync(ma.xstar, 0, n * nr * sizeof(double), h->stream));
+  // right-hand sides: [nr][m] from the caller -> [m][nr] interleaved; ||b_q||^2 per RHS
+  double* tmp = nullptr;
+  TRY(dalloc(h, &tmp, m * nr));
+  CK(h, cudaMemcpyAsync(tmp, b_all, m * nr * sizeof(double), cudaMemcpyDefault, h->stream));
+  k_interleave<<<nblocks(m * nr, 256, 4096), 256, 0, h->stream>>>(tmp, ma.b, m, nr, 1);
+  std::vector<double> hb(m * nr);
+  CK(h, cudaMemcpyAsync(hb.data(), tmp, m * nr * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  std::vector<double> bn(nr, 0.0);
+  for (int q = 0; q < nr; ++q)
+    for (long long i = 0; i < m; ++i) {
+      const double t = hb[q * m + i];
+      if (!std::isfinite(t)) return set_err(h, RGDBEK_E_NONFINITE, "NaN or Inf in b (right-hand side %d)", q);
+      bn[q] += t * t;
+    }
+  for (int q = 0; q < nr; ++q)
+    if (!(bn[q] > 0.0)) return set_err(h, RGDBEK_E_ZERO_RHS, "||b_%d|| == 0: RSE is undefined (P:301-304)", q);
+  for (int q = 0; q < nr; ++q) {
+    TRY(dalloc(h, &ma.keys_n[q], n));
+    TRY(dalloc(h, &ma.keys_m[q], m));
+    TRY(dalloc(h, &ma.hist[q], 6 * NBINS));
+    TRY(dalloc(h, &ma.cand[q], 2 * CAND_CAP));
+    TRY(dalloc(h, &ma.acc[q], 4));
+    TRY(dalloc(h, &ma.ncand[q], 2));
+    CK(h, cudaMemsetAsync(ma.hist[q], 0, 6 * NBINS * sizeof(unsigned int), h->stream));
+    CK(h, cudaMemsetAsync(ma.acc[q], 0, 4 * sizeof(unsigned long long), h->stream));
+    CK(h, cudaMemsetAsync(ma.ncand[q], 0, 2 * sizeof(unsigned int), h->stream));
+    if (q == 0) {
+      ma.st[0] = h->st;
+      ma.tr[0] = h->trace;
+    } else {
+      TRY(dalloc(h, &ma.st[q], 1));
+      TRY(dalloc(h, &ma.tr[q], std::max<long long>(h->trace_cap, 1)));
+      CK(h, cudaMemsetAsync(ma.tr[q], 0, std::max<long long>(h->trace_cap, 1) * sizeof(TraceRec), h->stream));
+    }
+    CK(h, cudaMallocHost(&h->mst_host[q], sizeof(Scal)));
+    memcpy(h->mst_host[q], h->st_host, sizeof(Scal));
+    h->mst_host[q]->bnorm2 = bn[q];
+    CK(h, cudaMemcpyAsync(ma.st[q], h->mst_host[q], sizeof(Scal), cudaMemcpyHostToDevice, h->stream));
+  }
+  h->st_host->bnorm2 = bn[0];
+  h->bnorm2 = bn[0];
+  const void* kf = nr == 2 ? (const void*)k_multi<2> : nr == 3 ? (const void*)k_multi<3> : (const void*)k_multi<4>;
+  CK(h, cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->p_dyn));
+  int occ = 0;
+  CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, PT, h->p_dyn));
+  if (occ < 1) return set_err(h, RGDBEK_E_CUDA, "multi-RHS kernel cannot be resident");
+  h->nrhs = nr;
+  CK(h, cudaStreamSynchronize(h->stream));
+  return rgdbek_reset(h, 0);
+}
+
+rgdbek_status rhs_check(rgdbek_ctx* h, int32_t rhs) {
+  TRY(ensure_usable(h));
+  if (rhs < 0 || rhs >= h->nrhs) return set_err(h, RGDBEK_E_ARG, "rhs %d outside [0, %d)", rhs, h->nrhs);
+  return RGDBEK_OK;
+}
+
+// one RHS of an interleaved [len][nr] vector into a caller buffer (host or device)
+rgdbek_status rhs_copy_out(rgdbek_ctx* h, const double* inter, long long len, int q, double* out) {
+  double* tmp = nullptr;
+  CK(h, cudaMalloc(&tmp, len * h->nrhs * sizeof(double)));
+  k_interleave<<<nblocks(len * h->nrhs, 256, 4096), 256, 0, h->stream>>>(inter, tmp, len, h->nrhs, 0);
+  cudaError_t e = cudaMemcpyAsync(out, tmp + (long long)q * len, len * sizeof(double), cudaMemcpyDefault, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  cudaFree(tmp);
+  if (e != cudaSuccess) return set_err(h, RGDBEK_E_CUDA, "rhs copy: %s", cudaGetErrorString(e));
+  return RGDBEK_OK;
+}
+
+__global__ void k_put_rhs(double* inter, const double* src, long long len, int nr, int q) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x)
+    inter[i * nr + q] = src[i];
+}
+
+}  // namespace
+
+extern "C" {
+
+rgdbek_status rgdbek_create_csr_multi(rgdbek_handle* out, int64_t m, int64_t n, int64_t nnz,
+                                      const int64_t* row_ptr, const int32_t* col_idx,
+                                      const double* val, const double* b_all, int32_t nrhs,
+                                      const rgdbek_options* opts) {
+  if (nrhs < 1 || nrhs > MAXRHS) return set_err(nullptr, RGDBEK_E_ARG, "nrhs must lie in [1, %d]", MAXRHS);
+  if (opts && (opts->nccl_comm || (opts->row_begin >= 0 && opts->row_begin != 0) ||
+               (opts->row_end >= 0 && opts->row_end != m)))
+    return set_err(nullptr, RGDBEK_E_STATE, "multiple right-hand sides: single GPU, all rows");
+  TRY(rgdbek_create_csr(out, m, n, nnz, row_ptr, col_idx, val, b_all, opts));
+  if (nrhs == 1) return RGDBEK_OK;
+  rgdbek_ctx* h = *out;
+  rgdbek_status s = setup_multi(h, b_all, nrhs);
+  if (s != RGDBEK_OK) {
+    g_create_error = h->err;
+    rgdbek_destroy(h);
+    *out = nullptr;
+    return s;
+  }
+  return RGDBEK_OK;
+}
+
+int32_t rgdbek_rhs_count(rgdbek_handle h) { return h ? h->nrhs : 0; }
+
+rgdbek_status rgdbek_get_x_rhs(rgdbek_handle h, int32_t rhs, double* out_n) {
+  TRY(rhs_check(h, rhs));
+  if (!out_n) return set_err(h, RGDBEK_E_ARG, "NULL out");
+  if (h->nrhs == 1) return rgdbek_get_x(h, out_n);
+  return rhs_copy_out(h, h->margs.x, h->n, rhs, out_n);
+}
+
+rgdbek_status rgdbek_get_z_rhs(rgdbek_handle h, int32_t rhs, double* out_m) {
+  TRY(rhs_check(h, rhs));
+  if (!out_m) return set_err(h, RGDBEK_E_ARG, "NULL out");
+  if (h->nrhs == 1) return rgdbek_get_z(h, out_m);
+  return rhs_copy_out(h, h->margs.z, h->m_loc, rhs, out_m);
+}
+
+rgdbek_status rgdbek_set_reference_rhs(rgdbek_handle h, int32_t rhs, const double* xstar) {
+  TRY(rhs_check(h, rhs));
+  if (!xstar) return set_err(h, RGDBEK_E_ARG, "NULL xstar");
+  if (h->nrhs == 1) return rgdbek_set_reference(h, xstar);
+  std::vector<double> hx(h->n);
+  CK(h, cudaMemcpy(hx.data(), xstar, h->n * sizeof(double), cudaMemcpyDefault));
+  double nrm = 0.0;
+  for (double t : hx) nrm += t * t;
+  if (!(nrm > 0.0) || !std::isfinite(nrm)) return set_err(h, RGDBEK_E_ARG, "||x*|| must be finite and > 0");
+  double* tmp = nullptr;
+  TRY(dalloc(h, &tmp, h->n));
+  CK(h, cudaMemcpyAsync(tmp, hx.data(), h->n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  k_put_rhs<<<nblocks(h->n, 256, 4096), 256, 0, h->stream>>>(h->margs.xstar, tmp, h->n, h->nrhs, rhs);
+  const int one = 1;
+  CK(h, cudaMemcpyAsync(&h->margs.st[rhs]->xsnorm2, &nrm, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(&h->st->has_ref, &one, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  // REL_ERR needs every RHS's reference
+  h->ref_mask |= 1u << rhs;
+  h->has_ref = h->ref_mask == (1u << h->nrhs) - 1u;
+  return RGDBEK_OK;
+}
+
+rgdbek_status rgdbek_get_trace_rhs(rgdbek_handle h, int32_t rhs, rgdbek_trace_record* out,
+                                   int64_t max_records, int64_t* n_out) {
+  TRY(rhs_check(h, rhs));
+  if (h->nrhs == 1) return rgdbek_get_trace(h, out, max_records, n_out);
+  if (!out || !n_out || max_records < 0) return set_err(h, RGDBEK_E_ARG, "bad arguments");
+  CK(h, cudaMemcpyAsync(h->st_host, h->st, sizeof(Scal), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  const long long k = h->st_host->k, cap = h->trace_cap;
+  if (cap <= 0) { *n_out = 0; return RGDBEK_OK; }
+  const long long first = std::max(0LL, k - cap);
+  const long long cnt = std::min<long long>(k - first, max_records);
+  std::vector<TraceRec> all(cap);
+  CK(h, cudaMemcpy(all.data(), h->margs.tr[rhs], cap * sizeof(TraceRec), cudaMemcpyDeviceToHost));
+  for (long long i = 0; i < cnt; ++i) {
+    memcpy(&out[i], &all[(first + i) % cap], sizeof(TraceRec));
+    out[i].k = first + i;
+  }
+  *n_out = cnt;
+  return RGDBEK_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
 
 // ===========================================================================
 // Peer-memory sharded engine: ownership plan, emulated groups, real peers
