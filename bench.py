@@ -293,6 +293,41 @@ def sparse_record(args, local, torch, peak, peak_src):
             "phases_us_per_iter": ph}
 
 
+def multi_rhs_record(args, local, torch, peak, nr=3):
+    """NEXT #2: the C4 blur operator with nr right-hand sides in one solve
+    (rgdbek_create_csr_multi).  An iteration advances all nr solves; algorithmic bytes of
+    one iteration = both reads of A + nr x (32 B per row + 24 B per column)."""
+    from paper_2509_19267_b200 import Solver
+    from workloads import by_name
+    w = by_name("C4")
+    m, n = w.shape
+    rng = np.random.default_rng(0)
+    B = np.array([w.b] + [w.A @ np.clip(rng.random(n), 0, 1) for _ in range(nr - 1)])
+    stream = torch.cuda.current_stream()
+    s = Solver.from_scipy_multi(w.A, B, eta=w.eta, stream=stream.cuda_stream)
+    s.reset(0)
+    s.step(args.warmup)
+    s.reset(0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    s.step(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3
+    s.close()
+    value = args.steps / t
+    a_bytes = 12.0 * w.A.nnz + 4.0 * (m + 1)
+    b_iter = 2 * a_bytes + nr * (32.0 * m + 24.0 * n)
+    return {"workload": "C4", "nrhs": nr, "value": round(value, 3), "unit": UNIT,
+            "rhs_iterations_per_s": round(nr * value, 3), "steps": args.steps,
+            "ms_per_step": round(1e3 * t / args.steps, 5),
+            "roofline": {"bound": "hbm", "achieved": round(b_iter * value / 1e9, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(b_iter * value / 1e9 / peak, 4),
+                         "iteration_bytes": b_iter,
+                         "a_bytes_per_rhs_iteration": round(2 * a_bytes / nr, 1)}}
+
+
 def run_ours(args):
     import torch
     from workloads import by_name
@@ -324,12 +359,17 @@ def run_ours(args):
         if use_nccl:
             comm = init_nccl_comm(local)
     s = make_solver(w, local, stream.cuda_stream, rows, comm)
+    # Algorithm 2: on one GPU --lazy P logical processes; across peer-sharded GPUs every
+    # rank is one process (set before connecting)
+    lazy_arg = (1 if args.lazy else 0) if (world > 1 and not use_nccl) else args.lazy
     if world > 1 and not use_nccl:
+        if lazy_arg:
+            s.set_lazy(1)
         from paper_2509_19267_b200.dist import connect_peers
         connect_peers(s)
     if args.mode == "exact":
         s.set_mode("exact", inner_tol=args.inner_tol, inner_max=args.inner_max)
-    if args.lazy:
+    if args.lazy and not (world > 1 and not use_nccl):
         s.set_lazy(args.lazy)
     engine, ctas = s.engine_info()
     s.reset(0)
@@ -354,6 +394,7 @@ def run_ours(args):
     value = args.steps / t                           # iterations of the one (sharded) system
     launches = 1 + (1 if engine == 0 else s.launches_per_iteration() * (args.steps + 1))
     npass = s.passes() if engine == 0 else 2 * (args.steps + 1)   # passes over A in the timed call
+    a_bytes_exact = s.a_bytes() if args.mode == "exact" else 0.0
 
     # roofline of the dominant kernel.  Persistent engine: the timed region IS one
     # launch of k_persistent (K iterations); achieved = K * B_iter / event time.
@@ -369,8 +410,9 @@ def run_ours(args):
         # exact mode: the inner solves make the passes per iteration data-dependent;
         # algorithmic bytes = (passes run) x (bytes of A per pass) + the vector sweeps
         m_, n_ = w.shape
-        a_pass = 8.0 * m_ * n_ if w.dense else 12.0 * w.A.nnz + 4.0 * (m_ + 1)
-        b_launch = npass * a_pass + args.steps * (32.0 * m_ + 24.0 * n_)
+        # bytes of A the launch read (full passes, and the dense x-solve's row-masked
+        # passes over A^J only: rgdbek_get_a_bytes) + the vector sweeps
+        b_launch = a_bytes_exact + args.steps * (32.0 * m_ + 24.0 * n_)
         ach = b_launch / t / 1e9
         roofline = {"bound": "hbm", "kernel": f"k_persistent_exact ({ctas} CTAs x 1024 threads; "
                                               f"{args.steps} iterations, {npass} passes over A)",
@@ -429,11 +471,13 @@ def run_ours(args):
             s2 = make_solver(w, local, stream.cuda_stream, rows, comm,
                              A_host=A_h if w.dense else None, b_host=b_h, csr_host=csr_h)
             if world > 1 and not use_nccl:
+                if lazy_arg:
+                    s2.set_lazy(1)
                 from paper_2509_19267_b200.dist import connect_peers
                 connect_peers(s2)
             if args.mode == "exact":
                 s2.set_mode("exact", inner_tol=args.inner_tol, inner_max=args.inner_max)
-            if args.lazy:
+            if args.lazy and not (world > 1 and not use_nccl):
                 s2.set_lazy(args.lazy)
             t1 = time.perf_counter()
             s2.reset(0)
@@ -466,6 +510,7 @@ def run_ours(args):
     if (world == 1 and not args.skip_sparse and w.dense and args.mode == "pinv_free"
             and not args.lazy):
         sparse = sparse_record(args, local, torch, peak, peak_src)
+        sparse["multi_rhs"] = multi_rhs_record(args, local, torch, peak)
     if comm is not None:
         from paper_2509_19267_b200.dist import destroy_nccl_comm
         destroy_nccl_comm(comm)
@@ -494,7 +539,9 @@ def run_ours(args):
                                        if world > 1 else "single"),
                        "engine": "persistent" if engine == 0 else "graph",
                        "update": args.mode,
-                       "algorithm": (f"Algorithm 2, {args.lazy} logical processes (lazy averaging)"
+                       "algorithm": ((f"Algorithm 2 across the {world} ranks (lazy averaging)"
+                                      if world > 1 and not use_nccl else
+                                      f"Algorithm 2, {args.lazy} logical processes (lazy averaging)")
                                      if args.lazy else "Algorithm 1"),
                        "l2": "inputs larger than L2 (A = %.0f MB > 126 MB)" % (
                            (m * n * 8 if w.dense else w.A.nnz * 12) / 1e6)},

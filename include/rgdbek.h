@@ -229,6 +229,9 @@ rgdbek_status rgdbek_engine_info(rgdbek_handle h, int32_t* engine, int32_t* ctas
 /* Full passes over A executed by the persistent engine since the last reset (2 per
  * iteration in mode 0; 2 + 2 per inner iteration in mode 1). */
 rgdbek_status rgdbek_get_counters(rgdbek_handle h, int64_t* passes);
+/* Exact mode (mode 1): algorithmic bytes of A read since the last reset — full passes
+ * count all of A, the dense x-solve's row-masked passes only the |J| rows of A^J. */
+rgdbek_status rgdbek_get_a_bytes(rgdbek_handle h, double* bytes);
 
 /* Block capture (test / diagnostics; SURVEY §8(c) parity protocol "full lists"): with
  * enable = 1 every later iteration also writes one byte per column and per local row

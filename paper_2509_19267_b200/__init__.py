@@ -227,6 +227,10 @@ class Solver:
         """Full passes over A since the last reset (persistent engine)."""
         return N.rgdbek_get_counters(self._h)
 
+    def a_bytes(self):
+        """Exact mode: algorithmic bytes of A read since the last reset."""
+        return N.rgdbek_get_a_bytes(self._h)
+
     def engine_info(self):
         """(engine, ctas): engine 0 = persistent kernel, 1 = CUDA-graph engine."""
         return N.rgdbek_engine_info(self._h)

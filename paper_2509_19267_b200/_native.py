@@ -24,7 +24,7 @@ EXPORTED = [
     "rgdbek_launch_kernel", "rgdbek_launches_per_iteration", "rgdbek_stream",
     "rgdbek_phase_times", "rgdbek_engine_info", "rgdbek_set_mode", "rgdbek_get_counters",
     "rgdbek_set_selection", "rgdbek_set_lazy", "rgdbek_set_capture", "rgdbek_selection_stats",
-    "rgdbek_build_info", "rgdbek_plan_ownership", "rgdbek_peer_window", "rgdbek_group_create",
+    "rgdbek_build_info", "rgdbek_get_a_bytes", "rgdbek_plan_ownership", "rgdbek_peer_window", "rgdbek_group_create",
     "rgdbek_group_reset", "rgdbek_group_step", "rgdbek_group_solve", "rgdbek_group_destroy",
     "rgdbek_peer_export", "rgdbek_peer_connect", "rgdbek_create_csr_multi", "rgdbek_rhs_count",
     "rgdbek_get_x_rhs", "rgdbek_get_z_rhs", "rgdbek_set_reference_rhs", "rgdbek_get_trace_rhs",
@@ -101,6 +101,7 @@ def load(path=None):
         "rgdbek_engine_info": (C.c_int, [H, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "rgdbek_set_mode": (C.c_int, [H, C.c_int32, C.c_double, C.c_int32]),
         "rgdbek_get_counters": (C.c_int, [H, C.POINTER(C.c_int64)]),
+        "rgdbek_get_a_bytes": (C.c_int, [H, C.POINTER(C.c_double)]),
         "rgdbek_set_selection": (C.c_int, [H, C.c_int32]),
         "rgdbek_set_lazy": (C.c_int, [H, C.c_int32]),
         "rgdbek_set_capture": (C.c_int, [H, C.c_int32]),
@@ -369,6 +370,12 @@ def rgdbek_peer_connect(h, nranks, rank, handles, windows):
 def rgdbek_get_counters(h):
     v = C.c_int64()
     check(load().rgdbek_get_counters(h, C.byref(v)), h)
+    return v.value
+
+
+def rgdbek_get_a_bytes(h):
+    v = C.c_double()
+    check(load().rgdbek_get_a_bytes(h, C.byref(v)), h)
     return v.value
 
 

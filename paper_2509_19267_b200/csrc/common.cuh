@@ -91,6 +91,7 @@ struct Scal {
   // persists across launches with the flag words) and the combined ||b||^2
   unsigned int xgen, pad3;
   double bnorm2_global;
+  double abytes;                 // exact mode: algorithmic bytes of A read since the last reset
 };
 
 constexpr int SURV_CAP = 256;    // per-rank survivors exchanged by allgather

@@ -27,9 +27,14 @@
 
 namespace rg {
 
+#ifndef RG_EX_MASK
+#define RG_EX_MASK 1        // dense x-solve passes read only the rows of A^J
+#endif
+
 struct EArgs {
   double inner_tol;
   int inner_max;
+  double bytesT, bytesN;   // algorithmic bytes of one full pass T / pass N over A
   double* px;      // Craig search direction (n)
   double* u;       // A px (m_loc)
 };
@@ -64,6 +69,111 @@ __device__ void ex_dense_colreduce(const PArgs& a, int use2, double* o1, double*
     }
     __syncthreads();
   }
+}
+
+// ---------------------------------------------------------------------------
+// Row-masked dense passes (the x-solve of the exact mode works on A^J only): rows outside
+// the row block J are not read at all, so an inner iteration of the x-solve streams
+// |J| / m of A instead of all of it.  Rows keep their order (a CTA compacts the selected
+// rows of each chunk by a block-wide prefix count), so the sums are deterministic.
+// ---------------------------------------------------------------------------
+// Selected rows of [r0, r0 + rows) in order -> rid[0..cnt); returns cnt (all threads).
+__device__ int ex_compact_rows(const PArgs& a, const PSel* rs, int r0, int rows, int* rid, int* wsum) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int total = 0;
+  for (int b0 = 0; b0 < rows; b0 += PT) {
+    const int i = b0 + threadIdx.x;
+    const bool sel = i < rows && p_selected(rs, a.keys_m[r0 + i], a.row0 + r0 + i);
+    const unsigned bal = __ballot_sync(0xffffffffu, sel);
+    __syncthreads();
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    int before = total;
+    for (int q = 0; q < w; ++q) before += wsum[q];
+    if (sel) rid[before + __popc(bal & ((1u << lane) - 1u))] = r0 + i;
+    int t = 0;
+    for (int q = 0; q < PW; ++q) t += wsum[q];
+    total += t;
+  }
+  __syncthreads();
+  return total;
+}
+
+// part[cta] = A^T in1 restricted to the selected rows of this CTA's row range.
+__device__ void ex_dense_passT_rows(const PArgs& a, const PSel* rs, const double* in1, double* smem) {
+  const int G = gridDim.x, bb = blockIdx.x;
+  const int rb = (int)((long long)a.m_loc * bb / G), re = (int)((long long)a.m_loc * (bb + 1) / G);
+  const int ntiles = (a.n + 2 * PT - 1) / (2 * PT);
+  double* zs = smem;                                         // [ZCH] values
+  int* rid = reinterpret_cast<int*>(smem + ZCH);             // [ZCH] row ids
+  int* wsum = rid + ZCH;                                     // [PW]
+  double* out = a.part + (long long)bb * 2 * a.n;
+  for (int t = 0; t < ntiles; ++t) {
+    const int c = t * 2 * PT + 2 * threadIdx.x;
+    double s0 = 0.0, s1 = 0.0;
+    for (int rc = rb; rc < re; rc += ZCH) {
+      const int rows = min(ZCH, re - rc);
+      __syncthreads();
+      const int cnt = ex_compact_rows(a, rs, rc, rows, rid, wsum);
+      for (int i = threadIdx.x; i < cnt; i += PT) zs[i] = in1[rid[i]];
+      __syncthreads();
+      if (c + 1 < a.n) {
+#pragma unroll 8
+        for (int i = 0; i < cnt; ++i) {
+          const double2 av = ld_stream2(a.A + (long long)rid[i] * a.lda + c);
+          s0 = fma(av.x, zs[i], s0);
+          s1 = fma(av.y, zs[i], s1);
+        }
+      } else if (c < a.n) {
+        for (int i = 0; i < cnt; ++i) s0 = fma(ld_stream(a.A + (long long)rid[i] * a.lda + c), zs[i], s0);
+      }
+    }
+    if (c + 1 < a.n) { out[c] = s0; out[c + 1] = s1; }
+    else if (c < a.n) out[c] = s0;
+  }
+}
+
+// out1 = A in1 on the selected rows of this CTA's row range (other rows untouched); one
+// warp per selected row, columns strided, fixed shuffle tree.  Returns nothing: the
+// caller forms its sums over J from out1.
+__device__ void ex_dense_passN_rows(const PArgs& a, const PSel* rs, const double* in1, double* out1,
+                                    double* smem) {
+  const int G = gridDim.x, bb = blockIdx.x;
+  const int rb = (int)((long long)a.m_loc * bb / G), re = (int)((long long)a.m_loc * (bb + 1) / G);
+  int* rid = reinterpret_cast<int*>(smem);
+  int* wsum = rid + ZCH;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int rc = rb; rc < re; rc += ZCH) {
+    const int rows = min(ZCH, re - rc);
+    __syncthreads();
+    const int cnt = ex_compact_rows(a, rs, rc, rows, rid, wsum);
+    for (int u = wid; u < cnt; u += PW) {
+      const double* ar = a.A + (long long)rid[u] * a.lda;
+      double acc = 0.0;
+      int c = lane * 2;
+      for (; c + 192 < a.n - 1; c += 256) {
+        double2 v[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) v[g] = ld_stream2(ar + c + 64 * g);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const double2 p = *reinterpret_cast<const double2*>(in1 + c + 64 * g);
+          acc = fma(v[g].x, p.x, acc);
+          acc = fma(v[g].y, p.y, acc);
+        }
+      }
+      for (; c + 1 < a.n; c += 64) {
+        const double2 v = ld_stream2(ar + c);
+        const double2 p = *reinterpret_cast<const double2*>(in1 + c);
+        acc = fma(v.x, p.x, acc);
+        acc = fma(v.y, p.y, acc);
+      }
+      if (c < a.n) acc = fma(ld_stream(ar + c), in1[c], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) out1[rid[u]] = acc;
+    }
+  }
+  __syncthreads();
 }
 
 // o1 = A^T in1 (and o2 = A^T in2 when use2) over all columns; ends after a grid barrier.
@@ -145,13 +255,17 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
   const double tol2 = e.inner_tol * e.inner_tol;
   unsigned int bgen = 0;
   if (threadIdx.x == 0) bgen = ld_acquire_u32(&a.bar->gen);
-  long long npass = 0;                       // full passes over A in this launch
+  long long npass = 0;                       // passes over A in this launch
+  // algorithmic bytes of A read in this launch: a full pass reads all of A, a row-masked
+  // dense x-solve pass only the |J| selected rows
+  double abytes = 0.0;
 
   // ---- prologue: A x_k (the first row step's residual and the RSE of x_k) ----
   double Yk;
   {
     double Wd = 0.0, Yp = 0.0;
     ++npass;
+    abytes += e.bytesN;
     ex_passN<DENSE>(a, ring, a.x, a.x, e.u, a.ax, a.b, Wd, Yp, dyn);
     double Wsum;
     ex_allsum2(a, Wd, Yp, SL_W, SL_Y, sh, bgen, Wsum, Yk);
@@ -162,6 +276,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
       st->halted = 1; st->outcome = RGDBEK_MAX_ITER; st->iters = k; st->rse_out = rse;
       st->relerr_out = __longlong_as_double(0x7FF8000000000000ll);
       st->npass += npass;
+      st->abytes += abytes;
     }
     return;
   }
@@ -171,6 +286,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
     __syncthreads();
     ++npass;
+    abytes += e.bytesT;
     ex_passT<DENSE>(a, ring, a.z, a.z, 0, a.s, a.v, dyn, bgen);                 // s = A^T z_k
     p_zero_side(a, 1);
     double Emax = 0.0;
@@ -237,6 +353,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     for (int it = 0; it < e.inner_max && kp > 0 && gam > 0.0; ++it) {
       double Wp = 0.0, Yd = 0.0;
       ++npass;
+      abytes += e.bytesN;
       ex_passN<DENSE>(a, ring, a.zeta, a.zeta, a.w, e.u, nullptr, Wp, Yd, dyn);           // q = A p
       double Wq, d2;
       ex_allsum2(a, Wp, 0.0, SL_W, SL_Y, sh, bgen, Wq, d2);
@@ -248,6 +365,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
       if (it + 1 == e.inner_max) break;
       grid_sync(a.bar, bgen);
       ++npass;
+      abytes += e.bytesT;
       ex_passT<DENSE>(a, ring, a.z, a.z, 0, a.s, a.v, dyn, bgen);                         // s' = A^T z
       double gp = 0.0;
       for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT)
@@ -335,7 +453,16 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     double V0 = 0.0;
     if (kpp > 0 && X > 0.0) {
       ++npass;
-      ex_passT<DENSE>(a, ring, a.xi, a.xi, 0, a.v, a.s, dyn, bgen);                      // t = A^T r_J
+      if constexpr (DENSE && RG_EX_MASK) {       // rows outside J hold r_J = 0: not read
+        ex_dense_passT_rows(a, &ps, a.xi, dyn);
+        grid_sync(a.bar, bgen);
+        ex_dense_colreduce(a, 0, a.v, a.s, dyn);
+        grid_sync(a.bar, bgen);
+        abytes += 8.0 * (double)kpp * (double)n;
+      } else {
+        abytes += e.bytesT;
+        ex_passT<DENSE>(a, ring, a.xi, a.xi, 0, a.v, a.s, dyn, bgen);                    // t = A^T r_J
+      }
       double gp = 0.0;
       for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) {
         const double t = a.v[j];
@@ -349,7 +476,13 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
       for (int it = 0; it < e.inner_max && gam > 0.0; ++it) {
         double Wd = 0.0, Yd = 0.0;
         ++npass;
-        ex_passN<DENSE>(a, ring, e.px, e.px, e.u, a.w, nullptr, Wd, Yd, dyn);            // u = A p
+        if constexpr (DENSE && RG_EX_MASK) {     // u is only used on J: A^J p
+          ex_dense_passN_rows(a, &ps, e.px, e.u, dyn);
+          abytes += 8.0 * (double)kpp * (double)n;
+        } else {
+          abytes += e.bytesN;
+          ex_passN<DENSE>(a, ring, e.px, e.px, e.u, a.w, nullptr, Wd, Yd, dyn);          // u = A p
+        }
         grid_sync(a.bar, bgen);   // sparse tiles spread rows over all CTAs
         double qp = 0.0;
         for (int i = blockIdx.x * PT + threadIdx.x; i < m_loc; i += G * PT)
@@ -366,7 +499,16 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
         if (it + 1 == e.inner_max) break;
         grid_sync(a.bar, bgen);
         ++npass;
-        ex_passT<DENSE>(a, ring, a.xi, a.xi, 0, a.v, a.s, dyn, bgen);                    // t = A^T r_J
+        if constexpr (DENSE && RG_EX_MASK) {
+          ex_dense_passT_rows(a, &ps, a.xi, dyn);
+          grid_sync(a.bar, bgen);
+          ex_dense_colreduce(a, 0, a.v, a.s, dyn);
+          grid_sync(a.bar, bgen);
+          abytes += 8.0 * (double)kpp * (double)n;
+        } else {
+          abytes += e.bytesT;
+          ex_passT<DENSE>(a, ring, a.xi, a.xi, 0, a.v, a.s, dyn, bgen);                  // t = A^T r_J
+        }
         double gq = 0.0;
         for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) gq += a.v[j] * a.v[j];
         double gnew, d7;
@@ -387,6 +529,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
     {
       double Wd = 0.0, Yp = 0.0, Rp = 0.0;
       ++npass;
+      abytes += e.bytesN;
       ex_passN<DENSE>(a, ring, a.x, a.x, e.u, a.ax, a.b, Wd, Yp, dyn);
       if (has_ref)
         for (int j = blockIdx.x * PT + threadIdx.x; j < n; j += G * PT) {
@@ -410,6 +553,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent_exact(PArgs a, EArgs e) {
         st->halted = 1; st->outcome = outcome; st->iters = k; st->rse_out = rse;
         st->relerr_out = rel; st->k = k; st->pending = 0; st->kp_prev = kp; st->kpp_prev = kpp;
         st->npass += npass;
+        st->abytes += abytes;
       }
       return;
     }

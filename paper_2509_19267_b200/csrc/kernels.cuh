@@ -648,6 +648,7 @@ __global__ void k_reset_scal(Scal* st, unsigned long long seed, long long k) {
   st->hash_acc = 0ull;
   st->error = 0;
   st->npass = 0;
+  st->abytes = 0.0;
   st->seln.mode = SEL_NONE;
   st->selm.mode = SEL_NONE;
   st->seln.ncand = st->selm.ncand = 0u;

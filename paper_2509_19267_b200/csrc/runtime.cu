@@ -1629,6 +1629,9 @@ rgdbek_status rgdbek_set_mode(rgdbek_handle h, int32_t mode, double inner_tol, i
     }
     h->eargs.inner_tol = inner_tol;
     h->eargs.inner_max = inner_max;
+    const double m_ = (double)h->m_loc, n_ = (double)h->n, z_ = (double)h->nnz;
+    h->eargs.bytesN = h->dense ? 8.0 * m_ * n_ : 12.0 * z_ + 8.0 * (m_ + 1);
+    h->eargs.bytesT = h->dense ? 8.0 * m_ * n_ : 12.0 * z_ + 8.0 * (n_ + 1);
   }
   h->mode = mode;
   return RGDBEK_OK;
@@ -1755,6 +1758,15 @@ int32_t rgdbek_build_info(int32_t* out, int32_t max_entries) {
   const int32_t c = max_entries < RGDBEK_BUILD_INFO_COUNT ? max_entries : RGDBEK_BUILD_INFO_COUNT;
   for (int32_t i = 0; i < c; ++i) out[i] = v[i];
   return c;
+}
+
+rgdbek_status rgdbek_get_a_bytes(rgdbek_handle h, double* bytes) {
+  TRY(ensure_usable(h));
+  if (!bytes) return set_err(h, RGDBEK_E_ARG, "NULL out");
+  CK(h, cudaMemcpyAsync(h->st_host, h->st, sizeof(Scal), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  *bytes = h->st_host->abytes;
+  return RGDBEK_OK;
 }
 
 rgdbek_status rgdbek_get_counters(rgdbek_handle h, int64_t* passes) {
