@@ -15,6 +15,17 @@
 namespace rg {
 
 constexpr int MAXRHS = 4;
+// gather entries per lane per round for NR = 2, 3, 4 right-hand sides (registers: the
+// gathered values are RU x 2 x NR doubles per lane)
+#ifndef RG_MRU2
+#define RG_MRU2 3
+#endif
+#ifndef RG_MRU3
+#define RG_MRU3 2
+#endif
+#ifndef RG_MRU4
+#define RG_MRU4 2
+#endif
 
 struct MArgs {
   int nr;                                 // right-hand sides
@@ -36,7 +47,7 @@ struct MArgs {
 template <int LV, int NR>
 __device__ __forceinline__ void tile_rows_m(const TileRows& t, double (&Wp)[NR], double (&Yp)[NR]) {
   constexpr int v = 1 << LV, spw = 32 >> LV;
-  constexpr int RU = NR == 1 ? RG_RU : (NR == 2 ? 3 : 2);
+  constexpr int RU = NR == 1 ? RG_RU : (NR == 2 ? RG_MRU2 : (NR == 3 ? RG_MRU3 : RG_MRU4));
   const int sub = t.lane >> LV, sl = t.lane & (v - 1);
   for (int base = t.lw * spw; base < t.nr; base += (TG / 32) * spw) {
     const int r = base + sub;
