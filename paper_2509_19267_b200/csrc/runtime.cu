@@ -2142,6 +2142,7 @@ rgdbek_status rgdbek_group_create(rgdbek_group* out, const rgdbek_handle* handle
   for (int r = 0; r < nranks; ++r) {
     rgdbek_ctx* h = g->h[r];
     sharded_fill(h, nranks, r, win.data(), ob.data());
+    h->sh.sys = 0;                        // every rank on this GPU: device-scope flag words
     for (int q = 0; q < nranks; ++q) sharded_peer(h->sh, q, g->h[q], static_cast<char*>(g->h[q]->arena));
     pg[r] = arena_gamma(g->h[r], static_cast<char*>(g->h[r]->arena));
   }
@@ -2239,6 +2240,7 @@ rgdbek_status rgdbek_peer_connect(rgdbek_handle h, int32_t nranks, int32_t rank,
     return set_err(h, RGDBEK_E_ARG, "windows[rank] differs from this rank's window");
   plan_ownership(nranks, win.data(), h->n, ob.data());
   sharded_fill(h, nranks, rank, win.data(), ob.data());
+  h->sh.sys = 1;                          // peers on other GPUs: system-scope flag words
   std::vector<const double*> pg(nranks);
   for (int q = 0; q < nranks; ++q) {
     char* base;

@@ -67,6 +67,7 @@ struct __align__(16) XComb {          // the rank-local sum over ranks (read by 
 // holds R of them, indexed by blockIdx.y).
 struct ShArgs {
   int R, rank;
+  int sys, pad_;                      // 1: ranks on different GPUs (system-scope flags)
   long long own0, own1;               // owned columns of this rank
   long long wlo, whi;                 // this rank's column window
   long long ownb[MAXR + 1];           // owned-column boundaries of every rank
@@ -82,12 +83,17 @@ struct ShArgs {
   GridBar* bar;                       // this rank's local grid barrier
 };
 
-__device__ __forceinline__ void st_release_sys_u32(unsigned int* p, unsigned int v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+// Flag words: system scope across GPUs (peers' memory over NVLink); an emulated group on
+// one GPU (ShArgs::sys == 0) needs only device scope, measured ~30 % cheaper per exchange
+// on the protocol (tools/sharded_probe.py, profiles/r2/sharded_probe_scope.jsonl).
+__device__ __forceinline__ void st_release_x_u32(unsigned int* p, unsigned int v, int sys) {
+  if (sys) asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+  else asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ unsigned int ld_acquire_sys_u32(const unsigned int* p) {
+__device__ __forceinline__ unsigned int ld_acquire_x_u32(const unsigned int* p, int sys) {
   unsigned int v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  if (sys) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -107,14 +113,15 @@ __device__ __forceinline__ void x_watch(unsigned int& spins, unsigned long long&
 // Signal round `rd` of exchange number `g` to every rank, then wait until every rank has.
 // Called by CTA 0 only, all threads.
 __device__ __forceinline__ void x_flags(const ShArgs& x, int rd, unsigned int g) {
-  __threadfence_system();              // this CTA's publish writes before the signal
+  if (x.sys) __threadfence_system();   // this CTA's publish writes before the signal
+  else __threadfence();
   __syncthreads();
-  if (threadIdx.x < x.R) st_release_sys_u32(&x.pflags[threadIdx.x]->arrive[rd][x.rank], g);
+  if (threadIdx.x < x.R) st_release_x_u32(&x.pflags[threadIdx.x]->arrive[rd][x.rank], g, x.sys);
   if (threadIdx.x < x.R) {
     const unsigned int* f = &x.pflags[x.rank]->arrive[rd][threadIdx.x];
     unsigned int spins = 0u;
     unsigned long long t0 = 0ull;
-    while ((int)(ld_acquire_sys_u32(f) - g) < 0) x_watch(spins, t0);
+    while ((int)(ld_acquire_x_u32(f, x.sys) - g) < 0) x_watch(spins, t0);
   }
   __syncthreads();
 }
@@ -525,7 +532,19 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
           __syncthreads();
         }
       }
-      // X, |J|, hash of the row step k-1 (formed in this pass T)
+    } else {
+      double d1 = 0.0, d2 = 0.0;
+      const int g = threadIdx.x / TG;
+      csr_tiles(blockIdx.x * (PT / TG) + g, G * (PT / TG), threadIdx.x % TG, 1 + g,
+                reinterpret_cast<TileSmem*>(dyn) + g, tring, a.cp, a.ri, a.rv, a.tilesT,
+                a.tilepT, a.ntilesT, a.z, a.xi, pending, nullptr, a.s, a.v, d1, d2, nullptr, 0,
+                a.vecT);
+      grid_sync(x.bar, bgen);
+    }
+    {
+      // every rank's window partials are complete after this global barrier, which also
+      // carries X, |J|, hash of the row step k-1 (dense: formed in this pass T; sparse:
+      // in the row-mask sweep that ended the previous iteration)
       XReq q = xreq();
       q.nslot = 1; q.slot[0] = SL_X;
       q.acc = a.acc + 2;
@@ -540,17 +559,6 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
         }
         kpp_prev = kppf;
       }
-    } else {
-      double d1 = 0.0, d2 = 0.0;
-      const int g = threadIdx.x / TG;
-      csr_tiles(blockIdx.x * (PT / TG) + g, G * (PT / TG), threadIdx.x % TG, 1 + g,
-                reinterpret_cast<TileSmem*>(dyn) + g, tring, a.cp, a.ri, a.rv, a.tilesT,
-                a.tilepT, a.ntilesT, a.z, a.xi, pending, nullptr, a.s, a.v, d1, d2, nullptr, 0,
-                a.vecT);
-      grid_sync(x.bar, bgen);
-      // the window partials of every rank are complete only after a global barrier
-      XReq q = xreq();
-      xsync(a, x, bgen, xg, q, sh_u, sh_l);
     }
     if constexpr (LAZY) x_zero_local(hm, a.ncand + 1);   // the rank's row selection is read
 
@@ -801,18 +809,7 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
       }
       const double xb = pblock_sum(Xp, sh);
       if (threadIdx.x == 0) bp[SL_X * G + blockIdx.x] = xb;
-      XReq q = xreq();
-      q.nslot = 1; q.slot[0] = SL_X;
-      q.acc = a.acc + 2;
-      xsync(a, x, bgen, xg, q, sh_u, sh_l);
-      X = cb->scal[0];
-      if (LAZY && threadIdx.x < x.R) lzX[threadIdx.x] = cb->rs[0][threadIdx.x];
-      const long long kpp = (long long)cb->acc[0];
-      if (lead) {
-        if (!LAZY && kpp != (ps.mode == SEL_NONE ? 0 : ps.target)) st->error |= 2;
-        if (TraceRec* t = trace_at(tr, st, k)) { t->kpp = kpp; t->hash_j = cb->acc[1]; t->X = X; }
-      }
-      kpp_prev = kpp;
+      // X, |J|, hash are published by the next iteration's first global barrier
     }
     kp_prev = kp;
     pending = 1;
