@@ -35,3 +35,14 @@ def test_pps_filter_denoises():
     for sp in r["species"]:
         assert sp["outcome"] == 0
         assert sp["rel_error_estimate"] < sp["rel_error_noisy"], sp
+
+
+def test_deblur_three_channels_as_three_right_hand_sides():
+    """The same deblurring with the channels as three right-hand sides of ONE solve
+    (multi-RHS, reading R29): the image is restored as well."""
+    from apps.drivers import deblur
+    r = deblur(side=64, iters=4000, multi_rhs=True)
+    assert r["multi_rhs"]
+    for ch in r["channels"]:
+        assert ch["psnr"] > ch["psnr_blurred"] + 5.0, ch
+        assert ch["ssim"] > 0.5, ch
