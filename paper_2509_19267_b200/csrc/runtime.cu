@@ -305,6 +305,23 @@ __global__ void k_gather_csc(const int* perm, const int* row_of, const double* v
   }
 }
 
+// ||v||^2 in a fixed order: block partials (grid-stride), then one block sums them.
+__global__ void k_sqnorm_part(const double* v, long long n, double* part) {
+  __shared__ double sh[8];
+  double t = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    t = fma(v[i], v[i], t);
+  t = block_sum<256>(t, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+__global__ void k_sqnorm_final(const double* part, int cnt, double* out) {
+  __shared__ double sh[8];
+  double t = 0.0;
+  for (int i = threadIdx.x; i < cnt; i += 256) t += part[i];
+  t = block_sum<256>(t, sh);
+  if (threadIdx.x == 0) *out = t;
+}
+
 __global__ void k_col_minmax(const int* ci, long long nnz, long long* mm /* [min, max] */) {
   long long lo = 0x7FFFFFFFFFFFFFFFll, hi = -1;
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
@@ -330,40 +347,83 @@ __global__ void k_compare(const long long* a, const long long* b, long long n1, 
 
 // Greedy row tiles over rows [r_begin, r_end): consecutive rows with <= TILE_NNZ nonzeros
 // and <= TILE_ROWS rows (a longer row is a tile by itself).  Tile ids are absolute rows.
+// Cut on the device: the rows are split into chunks of TILE_CHUNK rows, each chunk is
+// tiled greedily by one thread (tiles never cross a chunk start), a scan of the per-chunk
+// tile counts places every chunk's tiles — no copy of the row pointer to the host.
+constexpr long long TILE_CHUNK = 8192;
+
+template <bool WRITE>
+__global__ void k_tile_chunks(const long long* __restrict__ rp, long long r_begin, long long r_end,
+                              long long* __restrict__ count_or_offset, int* __restrict__ tiles,
+                              long long* __restrict__ tilep) {
+  const long long nch = (r_end - r_begin + TILE_CHUNK - 1) / TILE_CHUNK;
+  for (long long ch = (long long)blockIdx.x * blockDim.x + threadIdx.x; ch < nch;
+       ch += (long long)gridDim.x * blockDim.x) {
+    const long long c0 = r_begin + ch * TILE_CHUNK;
+    const long long c1 = c0 + TILE_CHUNK < r_end ? c0 + TILE_CHUNK : r_end;
+    long long out = WRITE ? count_or_offset[ch] : 0;
+    long long start = c0, acc = 0, cnt = 1;
+    if (WRITE) { tiles[out] = (int)c0; tilep[out] = rp[c0]; ++out; }
+    long long prev = rp[c0];
+    for (long long r = c0; r < c1; ++r) {
+      const long long next = rp[r + 1];
+      const long long len = next - prev;
+      if (r > start && (acc + len > TILE_NNZ || r - start >= TILE_ROWS)) {
+        if (WRITE) { tiles[out] = (int)r; tilep[out] = prev; ++out; }
+        ++cnt;
+        start = r;
+        acc = 0;
+      }
+      acc += len;
+      prev = next;
+    }
+    if (!WRITE) count_or_offset[ch] = cnt;
+  }
+}
+
+__global__ void k_tile_sentinel(const long long* rp, long long r_end, const long long* total,
+                                int* tiles, long long* tilep) {
+  tiles[*total] = (int)r_end;
+  tilep[*total] = rp[r_end];
+}
+
 rgdbek_status build_tiles(rgdbek_ctx* h, const long long* d_ptr, long long r_begin, long long r_end,
                           int** out, long long** outp, int* nt) {
   const long long rows = r_end - r_begin;
-  std::vector<long long> rpv(rows + 1);
-  CK(h, cudaMemcpyAsync(rpv.data(), d_ptr + r_begin, (rows + 1) * sizeof(long long),
-                        cudaMemcpyDeviceToHost, h->stream));
-  CK(h, cudaStreamSynchronize(h->stream));
-  const long long* rp = rpv.data() - r_begin;          // rp[r] for r in [r_begin, r_end]
-  std::vector<int> t;
-  t.push_back((int)r_begin);
-  long long start = r_begin, acc = 0;
-  for (long long r = r_begin; r < r_end; ++r) {
-    const long long len = rp[r + 1] - rp[r];
-    if (r > start && (acc + len > TILE_NNZ || r - start >= TILE_ROWS)) {
-      t.push_back((int)r);
-      start = r;
-      acc = 0;
-    }
-    acc += len;
+  if (rows <= 0) {                                     // an empty range: no tiles
+    int* d = nullptr;
+    long long* dp = nullptr;
+    TRY(dalloc(h, &d, 1));
+    TRY(dalloc(h, &dp, 1));
+    *out = d; *outp = dp; *nt = 0;
+    return RGDBEK_OK;
   }
-  if (rows > 0) t.push_back((int)r_end);
-  std::vector<long long> tp(t.size());
-  for (size_t i = 0; i < t.size(); ++i) tp[i] = rp[t[i]];
+  const long long nch = (rows + TILE_CHUNK - 1) / TILE_CHUNK;
+  long long* cnt = nullptr;                            // [nch + 1]: counts, then offsets
+  TRY(dalloc(h, &cnt, nch + 1));
+  const int gb = nblocks(nch, 128, 4096);
+  k_tile_chunks<false><<<gb, 128, 0, h->stream>>>(d_ptr, r_begin, r_end, cnt, nullptr, nullptr);
+  CK(h, cudaMemsetAsync(cnt + nch, 0, sizeof(long long), h->stream));
+  size_t tb = 0;
+  CK(h, cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, cnt, (int)(nch + 1), h->stream));
+  void* tbuf = nullptr;
+  CK(h, cudaMalloc(&tbuf, std::max<size_t>(tb, 1)));
+  CK(h, cub::DeviceScan::ExclusiveSum(tbuf, tb, cnt, cnt, (int)(nch + 1), h->stream));
+  long long total = 0;
+  CK(h, cudaMemcpyAsync(&total, cnt + nch, sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  cudaFree(tbuf);
   int* d = nullptr;
   long long* dp = nullptr;
-  TRY(dalloc(h, &d, t.size()));
-  TRY(dalloc(h, &dp, tp.size()));
-  CK(h, cudaMemcpyAsync(d, t.data(), t.size() * sizeof(int), cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(dp, tp.data(), tp.size() * sizeof(long long), cudaMemcpyHostToDevice,
-                        h->stream));
+  TRY(dalloc(h, &d, total + 1));
+  TRY(dalloc(h, &dp, total + 1));
+  k_tile_chunks<true><<<gb, 128, 0, h->stream>>>(d_ptr, r_begin, r_end, cnt, d, dp);
+  k_tile_sentinel<<<1, 1, 0, h->stream>>>(d_ptr, r_end, cnt + nch, d, dp);
+  CK(h, cudaGetLastError());
   CK(h, cudaStreamSynchronize(h->stream));
   *out = d;
   *outp = dp;
-  *nt = (int)t.size() - 1;
+  *nt = (int)total;
   return RGDBEK_OK;
 }
 
@@ -779,13 +839,16 @@ void setup_l2_window(rgdbek_ctx* h) {
 
 rgdbek_status finish_create(rgdbek_ctx* h) {
   if (h->dense) { h->wlo = 0; h->whi = h->n; }     // dense rows touch every column
-  // norms of b, block sizes (reading R2), scalar state, graph
-  std::vector<double> hb(h->m_loc);
-  CK(h, cudaMemcpyAsync(hb.data(), h->b, h->m_loc * sizeof(double), cudaMemcpyDeviceToHost,
-                        h->stream));
-  CK(h, cudaStreamSynchronize(h->stream));
+  // norms of b (on the device, fixed order), block sizes (reading R2), scalar state, graph
   double bn = 0.0;
-  for (double t : hb) bn += t * t;
+  {
+    double* part = nullptr;
+    TRY(dalloc(h, &part, 257));
+    k_sqnorm_part<<<256, 256, 0, h->stream>>>(h->b, h->m_loc, part);
+    k_sqnorm_final<<<1, 256, 0, h->stream>>>(part, 256, part + 256);
+    CK(h, cudaMemcpyAsync(&bn, part + 256, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+  }
   if (h->dist) {
     // sharded rows: gamma (column norms) and ||b||^2 are sums over ranks
     double* dbn = nullptr;
