@@ -41,9 +41,6 @@ namespace rg {
 #ifndef RG_REV_N
 #define RG_REV_N 1        // pass N walks the tiles / rows in reverse (L2 reuse after pass T)
 #endif
-#ifndef RG_TILE_BLOCKED
-#define RG_TILE_BLOCKED 0
-#endif
 #ifndef RG_TG
 #define RG_TG 256
 #endif
@@ -283,16 +280,11 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
                           double& Wp, double& Yp,
                           const ColKeyEpi* ep = nullptr, int acc1 = 0, int vec = 1,
                           int rev = 0) {
-  // default: tiles gid, gid + ngroups, ...: at any moment the groups of the
-  // whole GPU stream one contiguous window of the matrix (measured faster on C3
-  // than a contiguous run of tiles per group, RG_TILE_BLOCKED=1)
-#if RG_TILE_BLOCKED
-  const int tb = (int)((long long)ntiles * gid / ngroups), tstep = 1;
-  const int cnt = (int)((long long)ntiles * (gid + 1) / ngroups) - tb;
-#else
+  // tiles gid, gid + ngroups, ...: at any moment the groups of the whole GPU stream one
+  // contiguous window of the matrix (measured faster on C3 than a contiguous run of
+  // tiles per group: -12 %)
   const int tb = gid, tstep = ngroups;
   const int cnt = gid < ntiles ? (ntiles - gid + ngroups - 1) / ngroups : 0;
-#endif
   // the staging buffers may have been scratch of another phase (generic-proxy
   // writes): order those before the async-proxy (TMA) writes below
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -26,9 +26,6 @@ constexpr int ZCH = 1024;                 // rows of z / xi staged per chunk (pa
 #ifndef RG_VEC_PREFETCH2
 #define RG_VEC_PREFETCH2 1      // mask sweeps (P5, P11) pipelined too: C2c +1 %, C3 +2 %, C4 -2 %
 #endif
-#ifndef RG_P11_U4
-#define RG_P11_U4 0
-#endif
 #ifndef RG_SCAN_VU
 #define RG_SCAN_VU 6       // keys in flight per thread in the grid-wide level-2/3 scans (4: C3 -1.3 %)
 #endif
@@ -1521,32 +1518,6 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
         const bool sel = p_selected(&ps, ki, gi);
         a.xi[i] = sel ? ri : 0.0;
         if (sel) { Xp += ri * ri; cnt += 1; hs += splitmix64((unsigned long long)gi); }
-      }
-#elif RG_P11_U4
-      // four elements in flight per thread (8 independent loads), same per-thread order
-      const int i_beg = LAZY ? (int)((long long)m_loc * blockIdx.x / G) + threadIdx.x
-                             : blockIdx.x * PT + threadIdx.x;
-      const int i_end = LAZY ? (int)((long long)m_loc * (blockIdx.x + 1) / G) : m_loc;
-      const int step = LAZY ? PT : G * PT;
-      for (int i0 = i_beg; i0 < i_end; i0 += 4 * step) {
-        unsigned long long kv[4];
-        double rv[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int i = i0 + e * step;
-          kv[e] = i < i_end ? a.keys_m[i] : KEY_NEVER;
-          rv[e] = i < i_end ? a.r[i] : 0.0;
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int i = i0 + e * step;
-          if (i < i_end) {
-            const long long gi = a.row0 + i;
-            const bool sel = p_selected(&ps, kv[e], gi);
-            a.xi[i] = sel ? rv[e] : 0.0;
-                if (sel) { Xp += rv[e] * rv[e]; cnt += 1; hs += splitmix64((unsigned long long)gi); }
-          }
-        }
       }
 #else
       const int i_beg = LAZY ? (int)((long long)m_loc * blockIdx.x / G) + threadIdx.x

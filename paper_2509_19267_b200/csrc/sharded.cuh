@@ -40,8 +40,6 @@ constexpr int XSLOTS = 4;             // scalars published per barrier
 struct __align__(128) XFlags {
   unsigned int arrive[2][MAXR];       // [round][source rank]: last barrier the source reached
   unsigned int pad[32 - 2 * MAXR];
-  double bnorm2_local;                // ||b_r||^2 (combined in the kernel prologue)
-  double pad2[15];
 };
 
 struct __align__(16) XPub {           // one rank's contribution to one barrier
