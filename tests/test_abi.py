@@ -107,3 +107,19 @@ def test_build_info_reports_the_compiled_geometry(lib):
     assert info["tile_nnz"] >= info["tile_rows"] > 0
     assert info["local_sel_max"] == 32768 and info["final_cap"] == 1024
     assert info["persistent_threads"] == 1024 and info["tile_group_threads"] == 256
+
+
+def test_plan_ownership_host_only(lib):
+    """rgdbek_plan_ownership (no device): owned-column boundaries partition [0, n); banded
+    windows (strictly increasing) are split at the midpoint of each overlap, so every owned
+    column lies in its owner's window; identical windows (dense A) give equal slices."""
+    from paper_2509_19267_b200 import _native as N
+    n = 1000
+    wins = [(0, 270), (240, 520), (500, 760), (740, 1000)]
+    ob = N.rgdbek_plan_ownership(wins, n)
+    assert ob[0] == 0 and ob[-1] == n and all(ob[i] <= ob[i + 1] for i in range(4))
+    for r, (lo, hi) in enumerate(wins):
+        assert lo <= ob[r] and ob[r + 1] <= hi, (r, ob)
+    assert ob[1] == (240 + 270) // 2
+    assert N.rgdbek_plan_ownership([(0, n)] * 4, n) == [0, 250, 500, 750, 1000]
+    assert N.rgdbek_plan_ownership([(0, n)], n) == [0, n]
