@@ -39,6 +39,15 @@ def test_persistent_overflow_and_slow_paths():
     assert tot[1] > 0, out        # the exact slow path resolved selections
 
 
+def test_sharded_distributed_slow_path():
+    """The peer-sharded engine's distributed slow path (x_sel_slow: one radix level per
+    global exchange over every rank's keys) under the stress build, R = 2 and 4, dense and
+    sparse: full lists, x and z vs the oracle; the counter proves it ran."""
+    out = _variant_run("persistent", ["sharded:C5t:2", "sharded:C2s:4", "sharded:C3s:2"])
+    tot = np.sum([v for v in out["runs"].values()], axis=0)
+    assert tot[1] > 0, out
+
+
 def test_graph_engine_slow_path():
     out = _variant_run("graph", ["C1", "C3s"])
     tot = np.sum([v for v in out["runs"].values()], axis=0)
