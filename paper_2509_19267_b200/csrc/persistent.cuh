@@ -948,6 +948,8 @@ __device__ void p_csr(int vec, const long long* ptr, const int* idx, const doubl
 __device__ void p_zero_side(const PArgs& a, int side) {
   unsigned int* h = a.hist + side * 3 * NBINS;
   for (int i = blockIdx.x * PT + threadIdx.x; i < 3 * NBINS; i += gridDim.x * PT) h[i] = 0u;
+  unsigned int* hs = a.hist + (6 + side) * NBINS;               // the speculative level 2
+  for (int i = blockIdx.x * PT + threadIdx.x; i < NBINS; i += gridDim.x * PT) hs[i] = 0u;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.acc[2 * side] = 0ull;
     a.acc[2 * side + 1] = 0ull;
@@ -997,6 +999,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
   Cand* cm = a.cand + CAND_CAP;
   unsigned long long t_last = 0;
   unsigned int bgen = 0;
+  int predJ = -1;                               // speculative row level 2 (sparse, see P8)
   if (threadIdx.x == 0) bgen = ld_acquire_u32(&a.bar->gen);
 #define PH(i)                                                        \
   if (a.ptime && lead) {                                             \
@@ -1397,7 +1400,14 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
         return;
       }
     }
-    for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
+    // sparse, grid-wide row selection: a speculative level-2 histogram of the keys in the
+    // predicted level-1 bucket (the last iteration's), in the free tile memory
+    constexpr bool SPEC = !DENSE && !LAZY;
+    unsigned int* h2 = reinterpret_cast<unsigned int*>(dyn);
+    for (int i = threadIdx.x; i < NBINS; i += PT) {
+      h[i] = 0u;
+      if (SPEC) h2[i] = 0u;
+    }
     __syncthreads();
     double EmaxM = 0.0;
     {
@@ -1443,9 +1453,11 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
         const unsigned long long key = sel_key(eps, (unsigned long long)(a.row0 + i), k, 1u, seed, a.greedy);
         a.keys_m[i] = key;
         atomicAdd(&h[key >> L1_SHIFT], 1u);
+        if (SPEC && (int)(key >> L1_SHIFT) == predJ) atomicAdd(&h2[(key >> L2_SHIFT) & 0xFFFull], 1u);
       }
     }
     __syncthreads();
+    if (SPEC && predJ >= 0) flush_hist<PT>(h2, a.hist + 7 * NBINS, NBINS);
     if constexpr (LAZY) {
       flush_hist<PT>(h, a.lz_hist + (long long)(blockIdx.x / a.lzGp) * NBINS, NBINS);
     } else {
@@ -1484,11 +1496,18 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       PH(15);
     } else {
       p_sel_level1(&ps, hm, m_loc, kr, sh_u, sh_l);
-      p_sel_scan<2>(&ps, a.keys_m, m_loc, a.row0, hm + NBINS, cm, a.ncand + 1, h);
-      grid_sync(a.bar, bgen);
-      PH(8);
-      // ===== P10: level-2 bucket; level-3 scan + candidates =====
-      p_sel_level2(&ps, hm + NBINS, sh_u, sh_l);
+      const int d = ps.mode == SEL_PENDING ? (int)ps.prefix : -1;   // identical in every CTA
+      if (SPEC && d >= 0 && d == predJ) {
+        // speculation hit: the level-2 histogram was built with the keys (no scan, no barrier)
+        p_sel_level2(&ps, a.hist + 7 * NBINS, sh_u, sh_l);
+      } else {
+        p_sel_scan<2>(&ps, a.keys_m, m_loc, a.row0, hm + NBINS, cm, a.ncand + 1, h);
+        grid_sync(a.bar, bgen);
+        PH(8);
+        // ===== P10: level-2 bucket; level-3 scan + candidates =====
+        p_sel_level2(&ps, hm + NBINS, sh_u, sh_l);
+      }
+      if (SPEC) predJ = d;
       p_sel_scan<3>(&ps, a.keys_m, m_loc, a.row0, hm + 2 * NBINS, cm, a.ncand + 1, h);
       grid_sync(a.bar, bgen);
       PH(9);

@@ -726,12 +726,12 @@ rgdbek_status setup_persistent(rgdbek_ctx* h) {
   G = std::max(1LL, std::min<long long>(G, (long long)nsm * occ));
   G = std::min<long long>(G, MAXBLK);
   h->pG = (int)G;
-  TRY(dalloc(h, &h->phist, 6 * NBINS));
+  TRY(dalloc(h, &h->phist, 8 * NBINS));     // [2 sides][3 levels] + [2] speculative (sharded)
   TRY(dalloc(h, &h->pcand, 2 * CAND_CAP));
   TRY(dalloc(h, &h->pacc, 4));
   TRY(dalloc(h, &h->pncand, 2));
   TRY(dalloc(h, &h->pbar, 1));
-  CK(h, cudaMemsetAsync(h->phist, 0, 6 * NBINS * sizeof(unsigned int), h->stream));
+  CK(h, cudaMemsetAsync(h->phist, 0, 8 * NBINS * sizeof(unsigned int), h->stream));
   CK(h, cudaMemsetAsync(h->pacc, 0, 4 * sizeof(unsigned long long), h->stream));
   CK(h, cudaMemsetAsync(h->pncand, 0, 2 * sizeof(unsigned int), h->stream));
   CK(h, cudaMemsetAsync(h->pbar, 0, sizeof(GridBar), h->stream));

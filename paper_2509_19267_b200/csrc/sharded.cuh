@@ -47,6 +47,7 @@ struct __align__(16) XPub {           // one rank's contribution to one barrier
   unsigned long long acc[2];          // [count, hash] of a block
   unsigned int nsurv, sflag;          // level-3 survivors of this rank; overflow flag
   unsigned int hist[NBINS];
+  unsigned int hist2[NBINS];          // speculative level-2 histogram (predicted level-1 bucket)
   Cand surv[SURV_CAP];
 };
 
@@ -58,6 +59,7 @@ struct __align__(16) XComb {          // the rank-local sum over ranks (read by 
   long long below;
   unsigned int nsurv, sflag;
   unsigned int hist[NBINS];
+  unsigned int hist2[NBINS];
   Cand surv[MAXR * SURV_CAP];
 };
 
@@ -131,6 +133,7 @@ struct XReq {
   double direct;                      // nslot == -1: one direct value (prologue)
   unsigned long long* acc;            // rank-local [count, hash] to publish and zero (or null)
   unsigned int* hist;                 // rank-local histogram to publish and zero (or null)
+  unsigned int* hist2;                // a second one (the speculative level-2 histogram)
   // level-3 survivors (second exchange round): the rank-local candidate list of the
   // selection side and the selection state (identical in every CTA)
   const Cand* cand;
@@ -142,7 +145,8 @@ __device__ __forceinline__ XReq xreq() {
   XReq q;
   q.nslot = 0;
   q.direct = 0.0;
-  q.acc = nullptr; q.hist = nullptr; q.cand = nullptr; q.ncand = nullptr; q.ps = nullptr;
+  q.acc = nullptr; q.hist = nullptr; q.hist2 = nullptr; q.cand = nullptr; q.ncand = nullptr;
+  q.ps = nullptr;
   return q;
 }
 
@@ -201,6 +205,12 @@ __device__ void xsync(const PArgs& a, const ShArgs& x, unsigned int& bgen, unsig
       q.hist[i] = 0u;
     }
   }
+  if (q.hist2) {
+    for (int i = threadIdx.x; i < NBINS; i += PT) {
+      mine->hist2[i] = __ldcg(q.hist2 + i);
+      q.hist2[i] = 0u;
+    }
+  }
   x_flags(x, 0, xg);
   // ---- combine in rank order ----
   XComb* cb = x.comb;
@@ -223,6 +233,13 @@ __device__ void xsync(const PArgs& a, const ShArgs& x, unsigned int& bgen, unsig
       unsigned int t = 0u;
       for (int r = 0; r < x.R; ++r) t += __ldcv(&x.ppub[r][par].hist[i]);
       cb->hist[i] = t;
+    }
+  }
+  if (q.hist2) {
+    for (int i = threadIdx.x; i < NBINS; i += PT) {
+      unsigned int t = 0u;
+      for (int r = 0; r < x.R; ++r) t += __ldcv(&x.ppub[r][par].hist2[i]);
+      cb->hist2[i] = t;
     }
   }
   if (q.cand) {
@@ -359,26 +376,42 @@ __device__ void x_sel_slow(PSel* ps, const unsigned long long* __restrict__ keys
 
 // Exact global selection of the `kblock` smallest (key, index) over every rank's keys,
 // given this rank's level-1 histogram (already accumulated in gh[0..NBINS)).
-// Levels 2 and 3 scan the rank's own keys; three (or more) global barriers.
+// `first` is extra payload of the first exchange (its scalars come back in first_out /
+// first_rs); `gspec` is this rank's level-2 histogram of the keys whose level-1 digit is
+// `pred` (-1 = no speculation), built while the keys were made: when the level-1 bucket
+// is pred, the level-2 scan and its exchange are skipped.  digit_out = the resolved
+// level-1 bucket (-1 when no radix search ran).  Levels 2 and 3 scan the rank's own keys;
+// 2-3 global exchanges.
 __device__ void x_select(PSel* ps, const unsigned long long* __restrict__ keys, long long N_local,
                          long long idx_base, long long N_global, long long kblock, unsigned int* gh,
                          Cand* cand, unsigned int* ncand, unsigned int* h, const PArgs& a,
                          const ShArgs& x, unsigned int& bgen, unsigned int& xg, unsigned int* sh_u,
-                         long long* sh_l) {
+                         long long* sh_l, XReq first, double* first_out, double* first_rs,
+                         unsigned int* gspec, int pred, int& digit_out) {
+  digit_out = -1;
   {
-    XReq q = xreq();
+    XReq q = first;
     q.hist = gh;
+    if (pred >= 0) q.hist2 = gspec;
     xsync(a, x, bgen, xg, q, sh_u, sh_l);
+    if (first.nslot > 0) {
+      if (first_out) *first_out = x.comb->scal[0];
+      if (first_rs && threadIdx.x < x.R) first_rs[threadIdx.x] = x.comb->rs[0][threadIdx.x];
+    }
   }
   p_sel_level1(ps, x.comb->hist, N_global, kblock, sh_u, sh_l);
   if (ps->mode != SEL_PENDING) return;          // identical in every CTA of every rank
-  p_sel_scan<2>(ps, keys, N_local, idx_base, gh + NBINS, cand, ncand, h);
-  {
+  const int digit = (int)ps->prefix;            // the level-1 bucket
+  if (pred >= 0 && digit == pred) {
+    p_sel_level2(ps, x.comb->hist2, sh_u, sh_l);              // speculation hit
+  } else {
+    p_sel_scan<2>(ps, keys, N_local, idx_base, gh + NBINS, cand, ncand, h);
     XReq q = xreq();
     q.hist = gh + NBINS;
     xsync(a, x, bgen, xg, q, sh_u, sh_l);
+    p_sel_level2(ps, x.comb->hist, sh_u, sh_l);
   }
-  p_sel_level2(ps, x.comb->hist, sh_u, sh_l);
+  digit_out = digit;
   p_sel_scan<3>(ps, keys, N_local, idx_base, gh + 2 * NBINS, cand, ncand, h);
   {
     XReq q = xreq();
@@ -466,6 +499,10 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
   Cand* cn = a.cand;
   Cand* cm = a.cand + CAND_CAP;
   double* sown = LAZY ? a.lz_g : a.s;            // the owned columns' s = A^T z
+  unsigned int* hspec = a.hist + 6 * NBINS;      // speculative level-2 histograms [2][NBINS]
+  // speculative level-2 histograms: the predicted level-1 bucket is the last one
+  // (identical in every CTA of every rank); -1 = no speculation
+  int predU = -1, predJ = -1;
   unsigned int bgen = 0, xg = st->xgen;
   if (threadIdx.x == 0) bgen = ld_acquire_u32(&x.bar->gen);
   const XComb* cb = x.comb;
@@ -561,8 +598,9 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
     if constexpr (LAZY) x_zero_local(hm, a.ncand + 1);   // the rank's row selection is read
 
     // ===== P2: owned columns: s, v summed over the ranks whose window holds them;
-    //           column keys, level-1 histogram, V partial =====
-    for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
+    //           column keys, level-1 histogram (+ the speculative level-2 one), V partial =====
+    unsigned int* h2 = reinterpret_cast<unsigned int*>(dyn);       // free between the passes
+    for (int i = threadIdx.x; i < NBINS; i += PT) { h[i] = 0u; h2[i] = 0u; }
     __syncthreads();
     double Vp = 0.0;
     if constexpr (LAZY) {
@@ -592,29 +630,33 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
       const unsigned long long key = sel_key(eps, (unsigned long long)j, k, 0u, seed, 0);
       a.keys_n[j] = key;
       atomicAdd(&h[key >> L1_SHIFT], 1u);
+      if ((int)(key >> L1_SHIFT) == predU) atomicAdd(&h2[(key >> L2_SHIFT) & 0xFFFull], 1u);
     }
     __syncthreads();
     flush_hist<PT>(h, hn, NBINS);
+    if (predU >= 0) flush_hist<PT>(h2, hspec, NBINS);
     {
       const double vb = pblock_sum(Vp, sh);
       if (threadIdx.x == 0) bp[SL_V * G + blockIdx.x] = vb;
     }
-    double V;
+    // ===== P3-P5: the global column selection U (its first exchange also carries V) =====
+    __shared__ double Vsh;
     {
-      XReq q = xreq();
-      q.nslot = 1; q.slot[0] = SL_V;
-      xsync(a, x, bgen, xg, q, sh_u, sh_l);
-      V = cb->scal[0];
-      if (LAZY && threadIdx.x < x.R) lzV[threadIdx.x] = cb->rs[0][threadIdx.x];
+      XReq first = xreq();
+      first.nslot = 1; first.slot[0] = SL_V;
+      int d;
+      x_select(&ps, a.keys_n + own0, nown, own0, n, kc, hn, cn, a.ncand, h, a, x, bgen, xg, sh_u,
+               sh_l, first, threadIdx.x == 0 ? &Vsh : nullptr, LAZY ? lzV : nullptr, hspec, predU, d);
+      predU = d;                                    // speculate: the bucket repeats
+                                                    // (profiles/r2/sharded_probe_r2i_spec.jsonl)
     }
     __syncthreads();
+    const double V = Vsh;
     const int do_x = pending && kpp_prev > 0 && V > 0.0;
     const double alpha_x = do_x ? __ddiv_rn(X, V) : 0.0;
     if (lead && pending) {
       if (TraceRec* t = trace_at(tr, st, k - 1)) t->V = V;
     }
-    // ===== P3-P5: the global column selection U =====
-    x_select(&ps, a.keys_n + own0, nown, own0, n, kc, hn, cn, a.ncand, h, a, x, bgen, xg, sh_u, sh_l);
     if (lead && ps.slow) st->selstat[1] += 1;
     // |U|, hash and Z on owned columns (Algorithm 1: zeta = s on U); x_k; ||x - x*||^2
     {
@@ -757,7 +799,8 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
         return;
       }
     }
-    for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
+    unsigned int* h2m = reinterpret_cast<unsigned int*>(dyn);
+    for (int i = threadIdx.x; i < NBINS; i += PT) { h[i] = 0u; h2m[i] = 0u; }
     __syncthreads();
     {
       const int doz = kp > 0 && Wr > 0.0;
@@ -772,16 +815,20 @@ __global__ void __launch_bounds__(PT, 1) k_sharded(const PArgs* __restrict__ pa,
         const unsigned long long key = sel_key(eps, (unsigned long long)(a.row0 + i), k, 1u, seed, 0);
         a.keys_m[i] = key;
         atomicAdd(&h[key >> L1_SHIFT], 1u);
+        if (!LAZY && (int)(key >> L1_SHIFT) == predJ) atomicAdd(&h2m[(key >> L2_SHIFT) & 0xFFFull], 1u);
       }
     }
     __syncthreads();
     flush_hist<PT>(h, hm, NBINS);
+    if (!LAZY && predJ >= 0) flush_hist<PT>(h2m, hspec + NBINS, NBINS);
     // ===== P9-P11: the row selection J (Algorithm 2: this rank's own rows) =====
     if constexpr (LAZY) {
       x_select_local(&ps, a.keys_m, m_loc, a.row0, kr, hm, cm, a.ncand + 1, h, x, bgen, sh_u, sh_l);
     } else {
+      int d;
       x_select(&ps, a.keys_m, m_loc, a.row0, m_glob, kr, hm, cm, a.ncand + 1, h, a, x, bgen, xg,
-               sh_u, sh_l);
+               sh_u, sh_l, xreq(), nullptr, nullptr, hspec + NBINS, predJ, d);
+      predJ = d;
     }
     if (lead && ps.slow) st->selstat[1] += 1;
     if constexpr (!DENSE) {
