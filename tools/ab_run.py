@@ -1,7 +1,8 @@
 """A/B timing of library variants on one box (interleaved repetitions).
 
 usage: python tools/ab_run.py "C3,C4,C5s" base build_ab/librgdbek_x.so ... [--steps 300 --reps 2]
-'base' = the in-tree library.  Prints it/s per (variant, workload), median over reps.
+'base' = the in-tree library; 'env:K=V[,K2=V2]' = the in-tree library under those
+environment variables.  Prints it/s per (variant, workload), median over reps.
 """
 import json
 import os
@@ -37,7 +38,9 @@ def main():
     for _ in range(reps):
         for v in variants:
             env = dict(os.environ)
-            if v != "base":
+            if v.startswith("env:"):
+                env.update(kv.split("=", 1) for kv in v[4:].split(","))
+            elif v != "base":
                 env["RGDBEK_LIB"] = os.path.join(ROOT, v) if not os.path.isabs(v) else v
             for wl in wls:
                 out = subprocess.run([sys.executable, "-c", CHILD, wl, str(steps)], env=env,
@@ -49,7 +52,7 @@ def main():
                     it = float("nan")
                 res.setdefault((v, wl), []).append(it)
     for (v, wl), xs in res.items():
-        print(json.dumps({"variant": os.path.basename(v), "workload": wl,
+        print(json.dumps({"variant": v if v.startswith("env:") else os.path.basename(v), "workload": wl,
                           "it_s": round(statistics.median(xs), 1), "all": [round(x, 1) for x in xs]}))
 
 
