@@ -54,8 +54,15 @@ namespace rg {
 constexpr int TG = RG_TG;            // threads per worker group
 constexpr int TILE_NNZ = RG_TILE_NNZ;    // nonzeros per tile
 constexpr int TILE_ROWS = RG_TILE_ROWS;  // rows per tile
+#ifndef RG_GRAPH_TBUF
+// ring depth of the graph engine's standalone tile kernel: 2 buffers fit 6 blocks (48 tile
+// warps) per SM where 3 fit 4 — more consumer warps is what the sparse passes need
+// (C5c: graph engine 129 -> 135 it/s, C5m +6 %; profiles/r2/ab_engine_c5.jsonl)
+#define RG_GRAPH_TBUF 2
+#endif
 constexpr int TBUF = RG_TBUF;        // staged tiles per group (one in use, the rest in flight)
 constexpr int TRING = 2 * TBUF;      // ring words per group: full[TBUF] mbarriers, rel[TBUF] counters
+constexpr int GRAPH_TBUF = RG_GRAPH_TBUF;
 constexpr int PEND = RG_PEND;        // pass-T columns batched for the key epilogue
 static_assert(PEND >= TILE_ROWS, "a whole tile's columns must fit the pending list");
 
@@ -75,12 +82,14 @@ struct TilePend {
   int row[PEND];
 };
 
-struct __align__(16) TileSmem {
-  TileBuf buf[TBUF];
-  long long desc[TBUF][4];       // r0, r1, p0, p1 of the staged tile (written by the producer)
+template <int NB>
+struct __align__(16) TileSmemT {
+  TileBuf buf[NB];
+  long long desc[NB][4];         // r0, r1, p0, p1 of the staged tile (written by the producer)
   double red[2 * (TG / 32)];
   TilePend pend;
 };
+using TileSmem = TileSmemT<TBUF>;      // the persistent kernels' ring
 
 // Barrier over this worker group's TG threads (named barrier id >= 1).
 __device__ __forceinline__ void group_bar(int id) {
@@ -99,17 +108,19 @@ struct TileRing {
 
 // Initialise a group's barriers (one thread), before the first csr_tiles call;
 // the caller follows with fence.mbarrier_init + a CTA barrier.
+template <int NB = TBUF>
 __device__ __forceinline__ void tile_ring_init(unsigned long long* bars) {
-  for (int i = 0; i < TBUF; ++i) {
+  for (int i = 0; i < NB; ++i) {
     mbar_init(&bars[i], 1);
-    bars[TBUF + i] = 0ull;                         // release counter of buffer i
+    bars[NB + i] = 0ull;                           // release counter of buffer i
   }
 }
 
 // CTA prologue of a kernel running csr_tiles: every group's barriers, made
 // visible to the async proxy and to the whole CTA.
+template <int NB = TBUF>
 __device__ __forceinline__ void tile_rings_init(unsigned long long* bars) {
-  if (threadIdx.x % TG == 0) tile_ring_init(bars + (threadIdx.x / TG) * TRING);
+  if (threadIdx.x % TG == 0) tile_ring_init<NB>(bars + (threadIdx.x / TG) * (2 * NB));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
 }
@@ -128,7 +139,8 @@ __device__ __forceinline__ TileDesc tile_desc(int t, const int* __restrict__ til
 // goes to shared memory before the barrier's arrive (release), so consumers
 // read it after their wait (acquire).  Bytes are counted on the barrier
 // before the copies start (arrive.expect_tx).
-__device__ __forceinline__ void tile_issue(TileSmem* sm, int b, unsigned long long* bar,
+template <int NB>
+__device__ __forceinline__ void tile_issue(TileSmemT<NB>* sm, int b, unsigned long long* bar,
                                            const TileDesc& d, const long long* ptr,
                                            const int* idx, const double* val) {
   TileBuf* B = &sm->buf[b];
@@ -271,7 +283,9 @@ __device__ __forceinline__ void tile_rows(const TileRows& t, double& Wp, double&
   }
 }
 
-__device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm, TileRing& ring,
+// NB: ring depth (TBUF in the persistent kernels, GRAPH_TBUF in the graph engine's k_csr_tiles).
+template <int NB = TBUF>
+__device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmemT<NB>* sm, TileRing& ring,
                           const long long* __restrict__ ptr, const int* __restrict__ idx,
                           const double* __restrict__ val, const int* __restrict__ tiles,
                           const long long* __restrict__ tilep, int ntiles,
@@ -290,12 +304,12 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   group_bar(bar_id);
   unsigned long long* full = ring.full;
-  unsigned long long* rel = ring.full + TBUF;      // per-buffer count of warps done with it
+  unsigned long long* rel = ring.full + NB;      // per-buffer count of warps done with it
   if (lt == 0) {
-    for (int i = 0; i < cnt && i < TBUF; ++i) {
+    for (int i = 0; i < cnt && i < NB; ++i) {
       const unsigned u = ring.used + i;
       const int ti = tb + i * tstep;
-      tile_issue(sm, u % TBUF, &full[u % TBUF], tile_desc(rev ? ntiles - 1 - ti : ti, tiles, tilep),
+      tile_issue(sm, u % NB, &full[u % NB], tile_desc(rev ? ntiles - 1 - ti : ti, tiles, tilep),
                  ptr, idx, val);
     }
   }
@@ -305,16 +319,16 @@ __device__ void csr_tiles(int gid, int ngroups, int lt, int bar_id, TileSmem* sm
   int npend = 0;                                   // pass T: columns awaiting their keys
   for (int i = 0; i < cnt; ++i) {
     const int t = tb + i * tstep;                  // (reversed below when rev)
-    const unsigned u = ring.used + i, bi = u % TBUF;
+    const unsigned u = ring.used + i, bi = u % NB;
     // every warp's lane 0 fetches the descriptor of the tile this buffer is
     // refilled with (the last warp to release the buffer issues the refill)
     TileDesc nd{0, 0, 0, 0};
-    const bool refill = lane == 0 && i + TBUF < cnt;
+    const bool refill = lane == 0 && i + NB < cnt;
     if (refill) {
-      const int tn = t + TBUF * tstep;
+      const int tn = t + NB * tstep;
       nd = tile_desc(rev ? ntiles - 1 - tn : tn, tiles, tilep);
     }
-    mbar_wait(&full[bi], (u / TBUF) & 1u);
+    mbar_wait(&full[bi], (u / NB) & 1u);
     const int r0 = (int)sm->desc[bi][0], nr = (int)(sm->desc[bi][1] - sm->desc[bi][0]);
     const long long p0 = sm->desc[bi][2], p1 = sm->desc[bi][3];
     if (ep && npend + nr > PEND) {                 // make room in the pending list

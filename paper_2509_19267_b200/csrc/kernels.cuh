@@ -260,14 +260,14 @@ __global__ void __launch_bounds__(NT) k_csr_tiles(const long long* __restrict__ 
   constexpr int GPB = NT / TG;                    // worker groups per block
   extern __shared__ __align__(16) unsigned char tsm_raw[];
   const int g = threadIdx.x / TG;
-  TileSmem* sm = reinterpret_cast<TileSmem*>(tsm_raw) + g;
+  TileSmemT<GRAPH_TBUF>* sm = reinterpret_cast<TileSmemT<GRAPH_TBUF>*>(tsm_raw) + g;
   __shared__ double sh[NT / 32];
-  __shared__ __align__(8) unsigned long long tbar[GPB * TRING];
-  tile_rings_init(tbar);
-  TileRing ring{tbar + g * TRING, 0u};
+  __shared__ __align__(8) unsigned long long tbar[GPB * 2 * GRAPH_TBUF];
+  tile_rings_init<GRAPH_TBUF>(tbar);
+  TileRing ring{tbar + g * 2 * GRAPH_TBUF, 0u};
   const int use2 = (MODE == 1) ? st->pending : 1;
   double Wp = 0.0, Yp = 0.0;
-  csr_tiles(blockIdx.x * GPB + g, gridDim.x * GPB, threadIdx.x % TG, 1 + g, sm, ring, ptr, idx,
+  csr_tiles<GRAPH_TBUF>(blockIdx.x * GPB + g, gridDim.x * GPB, threadIdx.x % TG, 1 + g, sm, ring, ptr, idx,
             val, tiles, tilep, ntiles, in1, in2, use2, MODE == 0 ? b : nullptr, o1, o2, Wp, Yp,
             nullptr, 0, vec, MODE == 0 ? RG_REV_N : 0);
   if (MODE == 1) return;

@@ -71,6 +71,7 @@ struct rgdbek_ctx {
   double* npart = nullptr;              // dense pass N chunk partials [Q][m_loc][2]
   int graph_mode = 0;                   // 0 = WHILE node, 1 = plain body graph, 2 = eager
   int engine = 0;                       // 0 = persistent cooperative kernel, 1 = graph engine
+  bool engine_auto = false;             // engine 1 picked for a large sparse system (see setup_persistent)
   int pG = 1;                           // persistent: CTAs
   size_t p_dyn = 0;                     // persistent: dynamic smem bytes
   bool graph_built = false;             // graph engine captured (lazily for engine 0)
@@ -473,7 +474,7 @@ void launch_passT(rgdbek_ctx* h) {
         h->A, h->lda, (int)h->m_loc, (int)h->n, h->R, h->z, h->xi, h->part, h->st);
   } else {
     k_csr_tiles<1><<<std::min((h->ntilesT + NT / TG - 1) / (NT / TG), h->tile_grid), NT,
-                     (NT / TG) * sizeof(TileSmem), h->stream>>>(
+                     (NT / TG) * sizeof(TileSmemT<GRAPH_TBUF>), h->stream>>>(
         h->cp, h->ri, h->rv, h->tilesT, h->tilepT, h->ntilesT, h->z, h->xi, nullptr, h->s, h->v, h->st,
         h->trace, h->bpart, h->vecT);
   }
@@ -491,7 +492,7 @@ void launch_passN(rgdbek_ctx* h) {
         h->npart, h->nQ, (int)h->m_loc, h->b, h->w, h->ax, h->st, h->trace, h->bpart);
   } else {
     k_csr_tiles<0><<<std::min((h->ntilesN + NT / TG - 1) / (NT / TG), h->tile_grid), NT,
-                     (NT / TG) * sizeof(TileSmem), h->stream>>>(
+                     (NT / TG) * sizeof(TileSmemT<GRAPH_TBUF>), h->stream>>>(
         h->rp, h->ci, h->cv, h->tilesN, h->tilepN, h->ntilesN, h->zeta, h->x, h->b, h->w, h->ax, h->st,
         h->trace, h->bpart, h->vecN);
   }
@@ -692,8 +693,21 @@ rgdbek_status ensure_graph(rgdbek_ctx* h) {
 
 // Persistent engine: geometry, buffers and the kernel argument block.
 rgdbek_status setup_persistent(rgdbek_ctx* h) {
+  // Engine: the persistent kernel, except for a large sparse system on one GPU, where the
+  // graph engine's standalone tile kernels (2-deep rings, 6 blocks = 48 tile warps per SM
+  // against the persistent kernel's 32) outweigh its ~14 launches per iteration:
+  // nnz >= 2^26 (C5c 119.7 -> 135.3 it/s, C5m 1148 -> 1196; C3 / C4 lose 9 % and stay
+  // persistent; profiles/r2/ab_engine_c5.jsonl).  A feature only the persistent kernels
+  // implement switches back (prefer_persistent).  RGDBEK_ENGINE = graph | persistent.
+  long long graph_nnz = 1LL << 26;
+  if (const char* e = getenv("RGDBEK_GRAPH_NNZ")) graph_nnz = atoll(e);
+  if (!h->dense && !h->peer && !h->dist && h->nnz >= graph_nnz) {
+    h->engine = 1;
+    h->engine_auto = true;
+  }
   if (const char* e = getenv("RGDBEK_ENGINE")) {
-    if (!strcmp(e, "graph")) h->engine = 1;
+    if (!strcmp(e, "graph")) { h->engine = 1; h->engine_auto = false; }
+    if (!strcmp(e, "persistent") && !h->dist) { h->engine = 0; h->engine_auto = false; }
   }
   int nsm = 148, occ = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
@@ -1432,7 +1446,7 @@ rgdbek_status rgdbek_create_csr(rgdbek_handle* out, int64_t m, int64_t n, int64_
   {
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
-    const int tsm = (int)((NT / TG) * sizeof(TileSmem));
+    const int tsm = (int)((NT / TG) * sizeof(TileSmemT<GRAPH_TBUF>));
     cudaFuncSetAttribute(k_csr_tiles<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
     cudaFuncSetAttribute(k_csr_tiles<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_tiles<0>, NT, tsm);
@@ -1669,8 +1683,19 @@ rgdbek_status rgdbek_phase_times(rgdbek_handle h, double* out_ns, int32_t max_ph
   return RGDBEK_OK;
 }
 
+// The graph engine was picked automatically (large sparse system): a feature that only the
+// persistent kernels implement (exact mode, greedy sets, Algorithm 2, several right-hand
+// sides) switches the handle back to the persistent engine.
+static void prefer_persistent(rgdbek_ctx* h) {
+  if (h->engine_auto) {
+    h->engine = 0;
+    h->engine_auto = false;
+  }
+}
+
 rgdbek_status rgdbek_set_mode(rgdbek_handle h, int32_t mode, double inner_tol, int32_t inner_max) {
   TRY(ensure_usable(h));
+  if (mode == 1) prefer_persistent(h);
   if (mode != 0 && h->nrhs > 1)
     return set_err(h, RGDBEK_E_STATE, "multiple right-hand sides run the pseudoinverse-free update");
   if (mode != 0 && h->peer)
@@ -1704,6 +1729,7 @@ rgdbek_status rgdbek_set_mode(rgdbek_handle h, int32_t mode, double inner_tol, i
 rgdbek_status rgdbek_set_selection(rgdbek_handle h, int32_t selection) {
   TRY(ensure_usable(h));
   if (selection < 0 || selection > 1) return set_err(h, RGDBEK_E_ARG, "unknown selection rule %d", selection);
+  if (selection == 1) prefer_persistent(h);
   if (selection == 1 && (h->engine != 0 || h->dist || h->peer || h->nrhs > 1))
     return set_err(h, RGDBEK_E_STATE, "greedy selection runs on the single-GPU persistent engine");
   if (selection == 1 && h->lazyP)
@@ -1720,6 +1746,7 @@ rgdbek_status rgdbek_set_lazy(rgdbek_handle h, int32_t processes) {
   if (processes != 0 && h->nrhs > 1) return set_err(h, RGDBEK_E_STATE, "Algorithm 2 is not combined with multiple right-hand sides");
   if (processes < 0 || processes > LZ_MAX)
     return set_err(h, RGDBEK_E_ARG, "processes must lie in [0, %d]", LZ_MAX);
+  if (processes != 0) prefer_persistent(h);
   if (processes == 0) {                  // back to Algorithm 1
     if (h->peer && (h->group || h->connected)) return set_err(h, RGDBEK_E_STATE, "set the algorithm before grouping / connecting");
     h->lazyP = 0;
@@ -1892,6 +1919,7 @@ rgdbek_status rgdbek_nccl_comm_init(void** comm_out, int32_t nranks, int32_t ran
 namespace {
 
 rgdbek_status setup_multi(rgdbek_ctx* h, const double* b_all, int nr) {
+  prefer_persistent(h);
   if (h->dense || h->engine != 0 || h->dist || h->peer)
     return set_err(h, RGDBEK_E_STATE, "multiple right-hand sides run on the single-GPU persistent engine, sparse A");
   const long long n = h->n, m = h->m_loc;

@@ -2,7 +2,7 @@
 
 usage: python tools/ab_run.py "C3,C4,C5s" base build_ab/librgdbek_x.so ... [--steps 300 --reps 2]
 'base' = the in-tree library; 'env:K=V[,K2=V2]' = the in-tree library under those
-environment variables.  Prints it/s per (variant, workload), median over reps.
+environment variables; 'LIB|K=V[,K2=V2]' = a variant library under them.  Prints it/s per (variant, workload), median over reps.
 """
 import json
 import os
@@ -38,10 +38,13 @@ def main():
     for _ in range(reps):
         for v in variants:
             env = dict(os.environ)
-            if v.startswith("env:"):
-                env.update(kv.split("=", 1) for kv in v[4:].split(","))
-            elif v != "base":
-                env["RGDBEK_LIB"] = os.path.join(ROOT, v) if not os.path.isabs(v) else v
+            lib, _, envs = v.partition("|")          # "lib|K=V,..." = a library under env vars
+            if lib.startswith("env:"):
+                lib, envs = "base", lib[4:]
+            if envs:
+                env.update(kv.split("=", 1) for kv in envs.split(","))
+            if lib != "base":
+                env["RGDBEK_LIB"] = os.path.join(ROOT, lib) if not os.path.isabs(lib) else lib
             for wl in wls:
                 out = subprocess.run([sys.executable, "-c", CHILD, wl, str(steps)], env=env,
                                      capture_output=True, text=True, timeout=600)
@@ -52,7 +55,7 @@ def main():
                     it = float("nan")
                 res.setdefault((v, wl), []).append(it)
     for (v, wl), xs in res.items():
-        print(json.dumps({"variant": v if v.startswith("env:") else os.path.basename(v), "workload": wl,
+        print(json.dumps({"variant": v if ("env:" in v or "|" in v) else os.path.basename(v), "workload": wl,
                           "it_s": round(statistics.median(xs), 1), "all": [round(x, 1) for x in xs]}))
 
 
