@@ -12,6 +12,8 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -144,7 +146,8 @@ struct rgdbek_ctx {
   // errors
   int sticky = 0;
   std::string err;
-  std::vector<void*> allocs;
+  std::vector<void*> allocs;            // stream-ordered pool allocations (dalloc)
+  std::vector<void*> sync_allocs;       // cudaMalloc allocations (the IPC-exported peer arena)
 };
 
 namespace {
@@ -173,15 +176,43 @@ rgdbek_status set_err(rgdbek_ctx* h, rgdbek_status code, const char* fmt, ...) {
                      __LINE__);                                                            \
   } while (0)
 
+// Device memory comes from the device's stream-ordered memory pool with no release
+// threshold: a destroyed handle's memory stays mapped in the pool and the next create in
+// the process reuses it without driver calls (measured: cudaMalloc / cudaFree of the
+// ~1.5 GB of a C4 handle intermittently took 0.1-0.6 s on a fresh box, e2e creates
+// 31 ms -> 709 ms).  On an allocation failure the pool is trimmed and the call retried.
+cudaError_t pool_alloc(void** q, size_t bytes, cudaStream_t st, int device) {
+  static std::atomic<unsigned long long> ready{0};      // one bit per device: threshold set
+  if (device >= 0 && device < 64 && !(ready.load() >> device & 1ull)) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      unsigned long long thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    ready.fetch_or(1ull << device);
+  }
+  cudaError_t e = cudaMallocAsync(q, bytes, st);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      cudaStreamSynchronize(st);
+      cudaMemPoolTrimTo(pool, 0);
+      e = cudaMallocAsync(q, bytes, st);
+    }
+  }
+  return e;
+}
+
 template <typename T>
 rgdbek_status dalloc(rgdbek_ctx* h, T** p, size_t count) {
   void* q = nullptr;
   // 64 bytes of slack: the tile bulk copies widen their windows to 16-byte
   // boundaries and may read up to 16 bytes past the last element
   const size_t bytes = std::max<size_t>(count, 1) * sizeof(T) + 64;
-  cudaError_t e = cudaMalloc(&q, bytes);
+  cudaError_t e = pool_alloc(&q, bytes, h->stream, h->device);
   if (e != cudaSuccess)
-    return set_err(h, RGDBEK_E_OOM, "cudaMalloc(%zu bytes) failed: %s", bytes,
+    return set_err(h, RGDBEK_E_OOM, "device allocation (%zu bytes) failed: %s", bytes,
                    cudaGetErrorString(e));
   h->allocs.push_back(q);
   *p = static_cast<T*>(q);
@@ -193,6 +224,21 @@ rgdbek_status dalloc(rgdbek_ctx* h, T** p, size_t count) {
     rgdbek_status s_ = (x);         \
     if (s_ != RGDBEK_OK) return s_; \
   } while (0)
+
+// Create-time phase clock (RGDBEK_CREATE_TIMING=1): synchronizes the stream and prints the
+// wall time since the previous mark to stderr — a diagnostic of the e2e path only.
+struct CreateClock {
+  bool on = getenv("RGDBEK_CREATE_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(cudaStream_t st, const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "create: %-14s %9.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 inline int nblocks(long long work, int per_block, int cap) {
   long long b = (work + per_block - 1) / per_block;
@@ -409,12 +455,12 @@ rgdbek_status build_tiles(rgdbek_ctx* h, const long long* d_ptr, long long r_beg
   size_t tb = 0;
   CK(h, cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, cnt, (int)(nch + 1), h->stream));
   void* tbuf = nullptr;
-  CK(h, cudaMalloc(&tbuf, std::max<size_t>(tb, 1)));
+  CK(h, pool_alloc(&tbuf, std::max<size_t>(tb, 1), h->stream, h->device));
   CK(h, cub::DeviceScan::ExclusiveSum(tbuf, tb, cnt, cnt, (int)(nch + 1), h->stream));
   long long total = 0;
   CK(h, cudaMemcpyAsync(&total, cnt + nch, sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
-  cudaFree(tbuf);
+  cudaFreeAsync(tbuf, h->stream);
   int* d = nullptr;
   long long* dp = nullptr;
   TRY(dalloc(h, &d, total + 1));
@@ -925,7 +971,7 @@ rgdbek_status alloc_vectors(rgdbek_ctx* h) {
     h->arena_bytes = h->off_keys + up((size_t)n * sizeof(unsigned long long) + 64);
     cudaError_t e = cudaMalloc(&h->arena, h->arena_bytes);
     if (e != cudaSuccess) return set_err(h, RGDBEK_E_OOM, "cudaMalloc(arena) failed: %s", cudaGetErrorString(e));
-    h->allocs.push_back(h->arena);
+    h->sync_allocs.push_back(h->arena);
     CK(h, cudaMemsetAsync(h->arena, 0, h->arena_bytes, h->stream));
     char* base = static_cast<char*>(h->arena);
     h->s = reinterpret_cast<double*>(base + h->off_s);
@@ -1046,7 +1092,7 @@ rgdbek_status build_csc(rgdbek_ctx* h, long long** cp_out, int** ri_out, double*
   // temporaries (freed below)
   void* tmp[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   size_t nb = std::max<long long>(nnz, 1) * sizeof(int);
-  for (int t = 0; t < 5; ++t) CK(h, cudaMalloc(&tmp[t], nb));
+  for (int t = 0; t < 5; ++t) CK(h, pool_alloc(&tmp[t], nb, h->stream, h->device));
   row_of = (int*)tmp[0]; perm_in = (int*)tmp[1]; perm_out = (int*)tmp[2];
   key_in = (int*)tmp[3]; key_out = (int*)tmp[4];
   const int g = nblocks(nnz, 256, 4096);
@@ -1059,7 +1105,7 @@ rgdbek_status build_csc(rgdbek_ctx* h, long long** cp_out, int** ri_out, double*
   CK(h, cub::DeviceRadixSort::SortPairs(nullptr, tb, key_in, key_out, perm_in, perm_out, (int)nnz, 0,
                                         end_bit, h->stream));
   void* tbuf = nullptr;
-  CK(h, cudaMalloc(&tbuf, std::max<size_t>(tb, 1)));
+  CK(h, pool_alloc(&tbuf, std::max<size_t>(tb, 1), h->stream, h->device));
   CK(h, cub::DeviceRadixSort::SortPairs(tbuf, tb, key_in, key_out, perm_in, perm_out, (int)nnz, 0,
                                         end_bit, h->stream));
   // column counts -> exclusive scan -> col_ptr
@@ -1068,14 +1114,14 @@ rgdbek_status build_csc(rgdbek_ctx* h, long long** cp_out, int** ri_out, double*
   size_t sb = 0;
   CK(h, cub::DeviceScan::InclusiveSum(nullptr, sb, cp, cp, (int)(h->n + 1), h->stream));
   void* sbuf = nullptr;
-  CK(h, cudaMalloc(&sbuf, std::max<size_t>(sb, 1)));
+  CK(h, pool_alloc(&sbuf, std::max<size_t>(sb, 1), h->stream, h->device));
   CK(h, cub::DeviceScan::InclusiveSum(sbuf, sb, cp, cp, (int)(h->n + 1), h->stream));
   k_gather_csc<<<g, 256, 0, h->stream>>>(perm_out, row_of, h->cv, nnz, ri, rv);
   CK(h, cudaGetLastError());
   CK(h, cudaStreamSynchronize(h->stream));
-  for (int t = 0; t < 5; ++t) cudaFree(tmp[t]);
-  cudaFree(tbuf);
-  cudaFree(sbuf);
+  for (int t = 0; t < 5; ++t) cudaFreeAsync(tmp[t], h->stream);
+  cudaFreeAsync(tbuf, h->stream);
+  cudaFreeAsync(sbuf, h->stream);
   *cp_out = cp; *ri_out = ri; *rv_out = rv;
   return RGDBEK_OK;
 }
@@ -1286,7 +1332,9 @@ void rgdbek_destroy(rgdbek_handle h) {
   if (h->body_graph) cudaGraphDestroy(h->body_graph);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
-  for (void* p : h->allocs) cudaFree(p);
+  for (void* p : h->allocs) cudaFreeAsync(p, h->stream);
+  for (void* p : h->sync_allocs) cudaFree(p);
+  if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->st_host) cudaFreeHost(h->st_host);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -1376,10 +1424,12 @@ rgdbek_status rgdbek_create_csr(rgdbek_handle* out, int64_t m, int64_t n, int64_
   if (h->symmetric && m != n) { set_err(h, RGDBEK_E_ARG, "symmetric=1 needs a square A"); return create_fail(h, RGDBEK_E_ARG); }
   h->dense = false;
   h->nnz = nnz_local;
+  CreateClock clk;
   if ((s = dalloc(h, &h->rp, h->m_loc + 1)) != RGDBEK_OK) return create_fail(h, s);
   if ((s = dalloc(h, &h->ci, nnz_local)) != RGDBEK_OK) return create_fail(h, s);
   if ((s = dalloc(h, &h->cv, nnz_local)) != RGDBEK_OK) return create_fail(h, s);
   if ((s = alloc_vectors(h)) != RGDBEK_OK) return create_fail(h, s);
+  clk.mark(h->stream, "alloc");
   cudaError_t e = cudaMemcpyAsync(h->rp, row_ptr_local, (h->m_loc + 1) * sizeof(long long), cudaMemcpyDefault, h->stream);
   if (e == cudaSuccess && nnz_local > 0) e = cudaMemcpyAsync(h->ci, col_idx, nnz_local * sizeof(int), cudaMemcpyDefault, h->stream);
   if (e == cudaSuccess && nnz_local > 0) e = cudaMemcpyAsync(h->cv, val, nnz_local * sizeof(double), cudaMemcpyDefault, h->stream);
@@ -1390,6 +1440,7 @@ rgdbek_status rgdbek_create_csr(rgdbek_handle* out, int64_t m, int64_t n, int64_
   if (e == cudaSuccess) e = cudaMemcpyAsync(&ends[1], h->rp + h->m_loc, sizeof(long long), cudaMemcpyDeviceToHost, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) { set_err(h, RGDBEK_E_CUDA, "%s", cudaGetErrorString(e)); return create_fail(h, RGDBEK_E_CUDA); }
+  clk.mark(h->stream, "copy");
   if (ends[0] != 0 || ends[1] != nnz_local) {
     set_err(h, RGDBEK_E_CSR, "row_ptr[0] = %lld (expected 0), row_ptr[m] = %lld (expected nnz = %lld)", ends[0], ends[1], (long long)nnz_local);
     return create_fail(h, RGDBEK_E_CSR);
@@ -1402,9 +1453,11 @@ rgdbek_status rgdbek_create_csr(rgdbek_handle* out, int64_t m, int64_t n, int64_
   k_check_finite<<<nblocks(nnz_local, 256, 4096), 256, 0, h->stream>>>(h->cv, nnz_local, flag);
   k_check_finite<<<nblocks(h->m_loc, 256, 1024), 256, 0, h->stream>>>(h->b, h->m_loc, flag);
   if ((s = check_flag(h, flag, RGDBEK_E_NONFINITE, "NaN or Inf in A or b")) != RGDBEK_OK) return create_fail(h, s);
+  clk.mark(h->stream, "validate");
   // transposed copy for pass T (a stable radix sort by column keeps rows ordered)
   long long* cp = nullptr; int* ri = nullptr; double* rv = nullptr;
   if ((s = build_csc(h, &cp, &ri, &rv)) != RGDBEK_OK) return create_fail(h, s);
+  clk.mark(h->stream, "csc");
   if (h->symmetric) {
     cudaMemsetAsync(flag, 0, sizeof(int), h->stream);
     k_compare<<<nblocks(std::max<long long>(h->n + 1, nnz_local), 256, 4096), 256, 0, h->stream>>>(cp, h->rp, h->n + 1, ri, h->ci, rv, h->cv, nnz_local, flag);
@@ -1423,7 +1476,9 @@ rgdbek_status rgdbek_create_csr(rgdbek_handle* out, int64_t m, int64_t n, int64_
     const int v = atoi(e);
     if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) h->vecN = h->vecT = v;
   }
+  clk.mark(h->stream, "norms");
   if ((s = build_tiles(h, h->rp, 0, h->m_loc, &h->tilesN, &h->tilepN, &h->ntilesN)) != RGDBEK_OK) return create_fail(h, s);
+  clk.mark(h->stream, "tiles N");
   // the column window of the local rows: a peer-sharded rank's pass T tiles cover only it
   h->wlo = 0; h->whi = h->n;
   if (h->peer) {
@@ -1452,7 +1507,9 @@ rgdbek_status rgdbek_create_csr(rgdbek_handle* out, int64_t m, int64_t n, int64_
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_tiles<0>, NT, tsm);
     h->tile_grid = std::max(1, std::min(MAXBLK, nsm * std::max(occ, 1)));
   }
+  clk.mark(h->stream, "tiles T");
   if ((s = finish_create(h)) != RGDBEK_OK) return create_fail(h, s);
+  clk.mark(h->stream, "finish");
   *out = h;
   return RGDBEK_OK;
 }
@@ -2001,11 +2058,11 @@ rgdbek_status rhs_check(rgdbek_ctx* h, int32_t rhs) {
 // one RHS of an interleaved [len][nr] vector into a caller buffer (host or device)
 rgdbek_status rhs_copy_out(rgdbek_ctx* h, const double* inter, long long len, int q, double* out) {
   double* tmp = nullptr;
-  CK(h, cudaMalloc(&tmp, len * h->nrhs * sizeof(double)));
+  CK(h, pool_alloc((void**)&tmp, len * h->nrhs * sizeof(double), h->stream, h->device));
   k_interleave<<<nblocks(len * h->nrhs, 256, 4096), 256, 0, h->stream>>>(inter, tmp, len, h->nrhs, 0);
   cudaError_t e = cudaMemcpyAsync(out, tmp + (long long)q * len, len * sizeof(double), cudaMemcpyDefault, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-  cudaFree(tmp);
+  cudaFreeAsync(tmp, h->stream);
   if (e != cudaSuccess) return set_err(h, RGDBEK_E_CUDA, "rhs copy: %s", cudaGetErrorString(e));
   return RGDBEK_OK;
 }

@@ -22,8 +22,11 @@ else
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_persistent -c 1 -o gpurun_out/prof_${T}_$w python tools/run_steps.py $w 4 > gpurun_out/ncu_${T}_$w.log 2>&1; echo ncu_$w=$?
     summ gpurun_out/prof_${T}_$w
   done
+  # C5 runs the graph engine (nnz >= 2^26): its two tile kernels (pass T, pass N), and the
+  # launch list of a few iterations for the kernels' shares
   timeout 900 python tools/run_steps.py C5c 2 > /dev/null 2>&1 && \
-  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_persistent -c 1 -o gpurun_out/prof_${T}_C5c python tools/run_steps.py C5c 2 > gpurun_out/ncu_${T}_C5c.log 2>&1; echo ncu_C5c=$?
+  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_csr_tiles -c 2 -o gpurun_out/prof_${T}_C5c python tools/run_steps.py C5c 2 > gpurun_out/ncu_${T}_C5c.log 2>&1; echo ncu_C5c=$?
   summ gpurun_out/prof_${T}_C5c
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches_C5c.csv python tools/run_steps.py C5c 3 > gpurun_out/ncu_${T}_C5c_launch.log 2>&1; echo ncu_C5c_launch=$?
 fi
 du -sh gpurun_out
