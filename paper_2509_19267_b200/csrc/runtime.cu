@@ -413,17 +413,26 @@ __global__ void k_tile_chunks(const long long* __restrict__ rp, long long r_begi
     long long start = c0, acc = 0, cnt = 1;
     if (WRITE) { tiles[out] = (int)c0; tilep[out] = rp[c0]; ++out; }
     long long prev = rp[c0];
-    for (long long r = c0; r < c1; ++r) {
-      const long long next = rp[r + 1];
-      const long long len = next - prev;
-      if (r > start && (acc + len > TILE_NNZ || r - start >= TILE_ROWS)) {
-        if (WRITE) { tiles[out] = (int)r; tilep[out] = prev; ++out; }
-        ++cnt;
-        start = r;
-        acc = 0;
+    constexpr int B = 16;                          // row pointers loaded ahead (independent loads)
+    for (long long r0 = c0; r0 < c1; r0 += B) {
+      long long nx[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) nx[u] = r0 + u < c1 ? rp[r0 + u + 1] : 0;
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const long long r = r0 + u;
+        if (r >= c1) break;
+        const long long next = nx[u];
+        const long long len = next - prev;
+        if (r > start && (acc + len > TILE_NNZ || r - start >= TILE_ROWS)) {
+          if (WRITE) { tiles[out] = (int)r; tilep[out] = prev; ++out; }
+          ++cnt;
+          start = r;
+          acc = 0;
+        }
+        acc += len;
+        prev = next;
       }
-      acc += len;
-      prev = next;
     }
     if (!WRITE) count_or_offset[ch] = cnt;
   }
