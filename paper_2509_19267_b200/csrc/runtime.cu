@@ -201,6 +201,7 @@ cudaError_t pool_alloc(void** q, size_t bytes, cudaStream_t st, int device) {
       e = cudaMallocAsync(q, bytes, st);
     }
   }
+  if (e != cudaSuccess) cudaGetLastError();   // reported by the caller; do not leave it pending
   return e;
 }
 
