@@ -92,7 +92,8 @@ typedef struct {
   double  eta;              /* block fraction, in (0,1); default 0.5                    */
   int32_t stop;             /* rgdbek_stop used by rgdbek_solve; default RGDBEK_STOP_RSE        */
   int32_t device;           /* CUDA ordinal; default 0                                          */
-  void*   stream;           /* cudaStream_t to run on; NULL = a library-owned stream           */
+  void*   stream;           /* cudaStream_t to run on (must outlive the handle); NULL = a
+                               library-owned stream                                            */
   void*   nccl_comm;        /* ncclComm_t; NULL = single GPU                                    */
   int64_t row_begin;        /* this rank's first global row; -1 (default) = 0                   */
   int64_t row_end;          /* one past this rank's last global row; -1 (default) = m          */
@@ -337,6 +338,10 @@ rgdbek_status rgdbek_nccl_comm_init(void** comm_out, int32_t nranks, int32_t ran
 rgdbek_status rgdbek_nccl_comm_destroy(void* comm);
 
 const char*   rgdbek_last_error(rgdbek_handle h);
+/* Frees the handle.  Its device memory goes back to the device's stream-ordered memory pool
+ * (cudaFreeAsync on the handle's stream, which is synchronised; a caller-supplied
+ * options.stream must therefore still be valid here), where the next create of the process
+ * reuses it; NULL is a no-op. */
 void          rgdbek_destroy(rgdbek_handle h);
 
 #ifdef __cplusplus
