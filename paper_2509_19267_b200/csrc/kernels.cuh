@@ -543,17 +543,32 @@ __global__ void __launch_bounds__(NT) k_mask_m(const unsigned long long* __restr
   long long cnt = 0;
   unsigned long long hs = 0ull;
   if (selmask) selmask += (st->k & 1) * (long long)m_loc;      // parity of k (get_blocks)
-  for (int i = blockIdx.x * NT + threadIdx.x; i < m_loc; i += gridDim.x * NT) {
-    const long long gi = row0 + i;
-    const bool sel = is_selected(ss, keys[i], gi);
-    const double ri = r[i];
-    xi[i] = sel ? ri : 0.0;
-    if (sel) {
-      Xp += ri * ri;
-      cnt += 1;
-      hs += splitmix64((unsigned long long)gi);
+  // 4 rows in flight per thread (independent loads), visited in the same order
+  const long long stride = (long long)gridDim.x * NT;
+  for (long long i0 = (long long)blockIdx.x * NT + threadIdx.x; i0 < m_loc; i0 += 4 * stride) {
+    unsigned long long kk[4];
+    double rr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = i0 + u * stride;
+      kk[u] = i < m_loc ? keys[i] : 0ull;
+      rr[u] = i < m_loc ? r[i] : 0.0;
     }
-    if (selmask) selmask[i] = sel ? 1 : 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = i0 + u * stride;
+      if (i >= m_loc) break;
+      const long long gi = row0 + i;
+      const bool sel = is_selected(ss, kk[u], gi);
+      const double ri = rr[u];
+      xi[i] = sel ? ri : 0.0;
+      if (sel) {
+        Xp += ri * ri;
+        cnt += 1;
+        hs += splitmix64((unsigned long long)gi);
+      }
+      if (selmask) selmask[i] = sel ? 1 : 0;
+    }
   }
   cnt = warp_sum_ll(cnt);
   hs = warp_sum_u64(hs);

@@ -110,13 +110,22 @@ __global__ void __launch_bounds__(NT) k_select_pass(const unsigned long long* __
   constexpr int SD = (LEVEL == 2) ? L2_SHIFT : L3_SHIFT;
   const unsigned long long pre = ss->prefix;
   const long long stride = (long long)gridDim.x * NT;
-  for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < N; i += stride) {
-    const unsigned long long key = keys[i];
-    if ((key >> SF) == pre) {
-      atomicAdd(&h[(key >> SD) & 0xFFFull], 1u);
-      if (LEVEL == 3 && !(which && st->dist)) {
-        const unsigned int slot = atomicAdd(&ss->ncand, 1u);
-        if (slot < CAND_CAP) cand[slot] = Cand{key, idx_base + i};
+  // SCAN_U keys in flight per thread (independent loads), visited in the same order
+  constexpr int SCAN_U = 4;
+  for (long long i0 = (long long)blockIdx.x * NT + threadIdx.x; i0 < N; i0 += SCAN_U * stride) {
+    unsigned long long kk[SCAN_U];
+#pragma unroll
+    for (int u = 0; u < SCAN_U; ++u) kk[u] = i0 + u * stride < N ? keys[i0 + u * stride] : 0ull;
+#pragma unroll
+    for (int u = 0; u < SCAN_U; ++u) {
+      const long long i = i0 + u * stride;
+      const unsigned long long key = kk[u];
+      if (i < N && (key >> SF) == pre) {
+        atomicAdd(&h[(key >> SD) & 0xFFFull], 1u);
+        if (LEVEL == 3 && !(which && st->dist)) {
+          const unsigned int slot = atomicAdd(&ss->ncand, 1u);
+          if (slot < CAND_CAP) cand[slot] = Cand{key, idx_base + i};
+        }
       }
     }
   }
