@@ -172,6 +172,8 @@ struct ColKeyEpi {
   unsigned long long seed;
   int pending;
   int greedy;
+  unsigned int* spec;      // speculative level-2 histogram (global) of the keys whose level-1
+  int pred;                // digit is `pred` (the last iteration's bucket), or nullptr
 };
 
 __device__ __forceinline__ void colkey_epilogue(const ColKeyEpi* ep, int j, double sj, double vj,
@@ -182,6 +184,7 @@ __device__ __forceinline__ void colkey_epilogue(const ColKeyEpi* ep, int j, doub
   const unsigned long long key = sel_key(eps, (unsigned long long)j, ep->k, 0u, ep->seed, ep->greedy);
   ep->keys[j] = key;
   atomicAdd(&ep->hist[key >> L1_SHIFT], 1u);
+  if (ep->spec && (int)(key >> L1_SHIFT) == ep->pred) atomicAdd(&ep->spec[(key >> L2_SHIFT) & 0xFFFull], 1u);
 }
 
 // Row results of pass N / the exact mode: outputs and the W / ||b - A x||^2

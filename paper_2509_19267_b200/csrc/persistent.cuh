@@ -32,6 +32,9 @@ constexpr int ZCH = 1024;                 // rows of z / xi staged per chunk (pa
 #ifndef RG_FUSE_XI
 #define RG_FUSE_XI 1      // dense: xi = r on J formed while pass T stages its rows (no P11 sweep)
 #endif
+#ifndef RG_SPEC_U
+#define RG_SPEC_U 1       // sparse: speculative column level 2 built in pass T's key epilogue
+#endif
 constexpr int PN_RB = 256;                // max rows per batch (dense pass N)
 constexpr int PN_QMAX = 8;                // max column chunks per row (dense pass N)
 #ifndef RG_LOCAL_SEL_MAX
@@ -1000,6 +1003,7 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
   unsigned long long t_last = 0;
   unsigned int bgen = 0;
   int predJ = -1;                               // speculative row level 2 (sparse, see P8)
+  int predU = -1;                               // speculative column level 2 (sparse, pass T)
   if (threadIdx.x == 0) bgen = ld_acquire_u32(&a.bar->gen);
 #define PH(i)                                                        \
   if (a.ptime && lead) {                                             \
@@ -1169,7 +1173,10 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
     } else {
       for (int i = threadIdx.x; i < NBINS; i += PT) h[i] = 0u;
       __syncthreads();
-      const ColKeyEpi ep{a.gamma, a.keys_n, h, k, seed, pending, a.greedy};
+      // speculative column level 2: the keys in the last iteration's level-1 bucket are
+      // counted by their level-2 digit as they are made (global atomics; zeroed in P8)
+      const ColKeyEpi ep{a.gamma, a.keys_n, h, k, seed, pending, a.greedy,
+                         (RG_SPEC_U && predU >= 0) ? a.hist + 6 * NBINS : nullptr, predU};
       const int g = threadIdx.x / TG;
       csr_tiles(blockIdx.x * (PT / TG) + g, G * (PT / TG), threadIdx.x % TG, 1 + g,
                 reinterpret_cast<TileSmem*>(dyn) + g, tring, a.cp, a.ri, a.rv, a.tilesT,
@@ -1219,11 +1226,18 @@ __global__ void __launch_bounds__(PT, 1) k_persistent(PArgs a) {
       PH(14);
     } else {
       p_sel_level1(&ps, hn, n, kc, sh_u, sh_l);
-      p_sel_scan<2>(&ps, a.keys_n, n, 0, hn + NBINS, cn, a.ncand, h);
-      grid_sync(a.bar, bgen);
-      PH(3);
-      // ===== P4: level-2 bucket; level-3 scan + candidates =====
-      p_sel_level2(&ps, hn + NBINS, sh_u, sh_l);
+      const int dU = ps.mode == SEL_PENDING ? (int)ps.prefix : -1;  // identical in every CTA
+      if (!DENSE && !LAZY && RG_SPEC_U && dU >= 0 && dU == predU) {
+        // speculation hit: pass T built the level-2 histogram (no scan, no barrier)
+        p_sel_level2(&ps, a.hist + 6 * NBINS, sh_u, sh_l);
+      } else {
+        p_sel_scan<2>(&ps, a.keys_n, n, 0, hn + NBINS, cn, a.ncand, h);
+        grid_sync(a.bar, bgen);
+        PH(3);
+        // ===== P4: level-2 bucket; level-3 scan + candidates =====
+        p_sel_level2(&ps, hn + NBINS, sh_u, sh_l);
+      }
+      if (!DENSE && !LAZY) predU = dU;
       p_sel_scan<3>(&ps, a.keys_n, n, 0, hn + 2 * NBINS, cn, a.ncand, h);
       grid_sync(a.bar, bgen);
       PH(4);
