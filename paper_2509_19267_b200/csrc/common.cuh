@@ -49,7 +49,7 @@ struct SelState {
   int mode;
   int slow;                    // candidate overflow -> single-block slow path
   unsigned int ncand;
-  unsigned int pad_;
+  unsigned int spec_hit;       // graph engine: level-1 bucket == the predicted digit
 };
 
 // Last-block counters
@@ -92,6 +92,9 @@ struct Scal {
   unsigned int xgen, pad3;
   double bnorm2_global;
   double abytes;                 // exact mode: algorithmic bytes of A read since the last reset
+  // graph engine: level-1 digit predicted for each side's next selection (the last one's);
+  // the key kernel counts that bucket's keys by level-2 digit (speculative level 2)
+  int spec_pred[2];
 };
 
 constexpr int SURV_CAP = 256;    // per-rank survivors exchanged by allgather

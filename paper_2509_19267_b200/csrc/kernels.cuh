@@ -365,10 +365,12 @@ __global__ void __launch_bounds__(NT) k_nside(int n, const double* __restrict__ 
                                              const double* __restrict__ xslot,
                                              const double* __restrict__ gamma,
                                              unsigned long long* __restrict__ keys, Scal* st,
-                                             TraceRec* tr, unsigned int* gh, double* bpart) {
+                                             TraceRec* tr, unsigned int* gh, double* bpart,
+                                             unsigned int* spec) {
   if (st->halted) return;
   __shared__ __align__(16) unsigned int h[NBINS];
   __shared__ double sh[NT / 32];
+  const int pred = st->spec_pred[0];
   for (int b = threadIdx.x; b < NBINS; b += NT) h[b] = 0u;
   __syncthreads();
   const int pending = st->pending;
@@ -386,6 +388,7 @@ __global__ void __launch_bounds__(NT) k_nside(int n, const double* __restrict__ 
     const unsigned long long key = make_key(eps, (unsigned long long)j, k, 0u, seed);
     keys[j] = key;
     atomicAdd(&h[key >> L1_SHIFT], 1u);
+    if ((int)(key >> L1_SHIFT) == pred) atomicAdd(&spec[(key >> L2_SHIFT) & 0xFFFull], 1u);
   }
   __syncthreads();
   flush_hist<NT>(h, gh, NBINS);
@@ -405,6 +408,7 @@ __global__ void __launch_bounds__(NT) k_nside(int n, const double* __restrict__ 
     }
   }
   finalize_level1<NT>(&st->seln, gh, n, st->kc);
+  spec_decide<NT>(&st->seln, &st->spec_pred[0], spec);
 }
 
 // ---------------------------------------------------------------------------
@@ -486,9 +490,10 @@ __global__ void __launch_bounds__(NT) k_mside(int m_loc, long long row0, double*
                                              const double* __restrict__ rho,
                                              double* __restrict__ r,
                                              unsigned long long* __restrict__ keys, Scal* st,
-                                             unsigned int* gh) {
+                                             unsigned int* gh, unsigned int* spec) {
   if (st->halted) return;
   __shared__ __align__(16) unsigned int h[NBINS];
+  const int pred = spec ? st->spec_pred[1] : -2;   // no speculation when sharded (spec null)
   for (int q = threadIdx.x; q < NBINS; q += NT) h[q] = 0u;
   __syncthreads();
   const int doz = st->kp > 0 && st->W > 0.0;
@@ -508,12 +513,14 @@ __global__ void __launch_bounds__(NT) k_mside(int m_loc, long long row0, double*
     const unsigned long long key = make_key(eps, (unsigned long long)(row0 + i), k, 1u, seed);
     keys[i] = key;
     atomicAdd(&h[key >> L1_SHIFT], 1u);
+    if ((int)(key >> L1_SHIFT) == pred) atomicAdd(&spec[(key >> L2_SHIFT) & 0xFFFull], 1u);
   }
   __syncthreads();
   flush_hist<NT>(h, gh, NBINS);
   if (st->dist) return;                      // histogram is allreduced, then k_sel_fin
   if (!last_block(&st->counters[C_MSIDE])) return;
   finalize_level1<NT>(&st->selm, gh, m_loc, st->kr);
+  spec_decide<NT>(&st->selm, &st->spec_pred[1], spec);
 }
 
 // ---------------------------------------------------------------------------

@@ -87,6 +87,7 @@ struct rgdbek_ctx {
   unsigned long long* pacc = nullptr;   // persistent: [4]
   unsigned int* pncand = nullptr;       // persistent: [2]
   GridBar* pbar = nullptr;
+  unsigned int* spec_hist = nullptr;    // graph engine: speculative level-2 histograms [2][NBINS]
   // multi-GPU (row-sharded) state
   int nranks = 1, rank = 0;
   bool dist = false;
@@ -613,10 +614,14 @@ long long enqueue_body(rgdbek_ctx* h, cudaGraphConditionalHandle cond, int use_c
   }
   // sharded rows: [A_p^T z_p | A_p^T xi_p | X_p] summed over ranks in one call
   if (h->dist) nccl_allreduce(h, h->s, 2 * h->n + 1, NCCL_F64);
+  // speculative level 2 (spec_hist [2][NBINS]): the key kernels count the predicted
+  // level-1 bucket's keys by level-2 digit; on a hit the level-2 pass skips its scan
+  unsigned int* spec_n = h->spec_hist;
+  unsigned int* spec_m = h->dist ? nullptr : h->spec_hist + NBINS;   // sharded rows: no
   k_nside<<<gn, NT, 0, h->stream>>>((int)h->n, h->s, h->v, h->xslot, h->gamma, kn, h->st,
-                                    h->trace, h->hist, h->bpart); ++L;
+                                    h->trace, h->hist, h->bpart, spec_n); ++L;
   // the column selection is replicated: every rank holds the same s
-  k_select_pass<NT, 2><<<gsn, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0, h->hist, h->cand); ++L;
+  k_select_pass<NT, 2><<<gsn, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0, h->hist, h->cand, spec_n); ++L;
   k_select_pass<NT, 3><<<gsn, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0, h->hist, h->cand); ++L;
   k_select_slow<NT><<<1, NT, 0, h->stream>>>(kn, h->n, 0, h->st, 0); ++L;
   k_mask_n<<<gn, NT, 0, h->stream>>>(kn, h->s, h->v, h->zeta, h->x, h->xstar, h->capture ? h->selmask_n : nullptr, (int)h->n,
@@ -628,13 +633,13 @@ long long enqueue_body(rgdbek_ctx* h, cudaGraphConditionalHandle cond, int use_c
     k_passN_decide<<<1, 1, 0, h->stream>>>(h->st, h->trace); ++L;
   }
   k_mside<<<gm, NT, 0, h->stream>>>((int)h->m_loc, h->row0, h->z, h->w, h->ax, h->b, h->rho,
-                                    h->r, km, h->st, h->hist); ++L;
+                                    h->r, km, h->st, h->hist, spec_m); ++L;
   if (h->dist) {
     nccl_allreduce(h, h->hist, NBINS, NCCL_U32);
     k_sel_fin<NT><<<1, NT, 0, h->stream>>>(h->st, h->hist, 1); ++L;
   }
   k_select_pass<NT, 2><<<gsm, NT, 0, h->stream>>>(km, h->m_loc, h->row0, h->st, 1, h->hist,
-                                                  h->cand); ++L;
+                                                  h->cand, spec_m); ++L;
   if (h->dist) {
     nccl_allreduce(h, h->hist, NBINS, NCCL_U32);
     k_sel_fin<NT><<<1, NT, 0, h->stream>>>(h->st, h->hist, 2); ++L;
@@ -1010,6 +1015,8 @@ rgdbek_status alloc_vectors(rgdbek_ctx* h) {
   TRY(dalloc(h, &h->keys_m, m));
   TRY(dalloc(h, &h->bpart, 4 * MAXBLK));
   TRY(dalloc(h, &h->hist, NBINS));
+  TRY(dalloc(h, &h->spec_hist, 2 * NBINS));
+  CK(h, cudaMemsetAsync(h->spec_hist, 0, 2 * NBINS * sizeof(unsigned int), h->stream));
   TRY(dalloc(h, &h->cand, CAND_CAP));
   TRY(dalloc(h, &h->trace, std::max<long long>(h->trace_cap, 1)));
   CK(h, cudaMemsetAsync(h->hist, 0, NBINS * sizeof(unsigned int), h->stream));

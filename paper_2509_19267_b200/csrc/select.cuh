@@ -95,14 +95,38 @@ __device__ void finalize_level1(SelState* ss, unsigned int* gh, long long N, lon
   }
 }
 
-// Level 2 / 3 pass over all keys of the bucket resolved so far.
+// Speculative level 2 of the graph engine, decided by the last block of the key kernel
+// right after finalize_level1: a hit when the new level-1 bucket is the predicted digit
+// (the key kernel counted that bucket's keys into `spec` by level-2 digit); a miss zeroes
+// `spec` for the next build.  The prediction becomes the new bucket.
+template <int NT>
+__device__ void spec_decide(SelState* ss, int* pred, unsigned int* spec) {
+  __shared__ int hit;
+  if (threadIdx.x == 0) {
+    hit = ss->mode == SEL_PENDING && (long long)ss->prefix == (long long)*pred;
+    ss->spec_hit = hit ? 1u : 0u;
+    *pred = ss->mode == SEL_PENDING ? (int)ss->prefix : -1;
+  }
+  __syncthreads();
+  if (!hit)
+    for (int b = threadIdx.x; b < NBINS; b += NT) spec[b] = 0u;
+}
+
+// Level 2 / 3 pass over all keys of the bucket resolved so far.  spec (level 2 only, or
+// nullptr): the speculative level-2 histogram — on a hit the scan is skipped.
 template <int NT, int LEVEL>
 __global__ void __launch_bounds__(NT) k_select_pass(const unsigned long long* __restrict__ keys,
                                                     long long N, long long idx_base, Scal* st,
-                                                    int which, unsigned int* gh, Cand* cand) {
+                                                    int which, unsigned int* gh, Cand* cand,
+                                                    unsigned int* spec = nullptr) {
   if (st->halted) return;
   SelState* ss = which ? &st->selm : &st->seln;
   if (ss->mode != SEL_PENDING) return;
+  if (LEVEL == 2 && spec && ss->spec_hit) {
+    if (!last_block(&st->counters[C_SEL2N + (which ? (C_SEL2M - C_SEL2N) : 0)])) return;
+    finalize_level<NT>(ss, spec, L2_SHIFT);   // zeroes spec for the next build
+    return;
+  }
   __shared__ __align__(16) unsigned int h[NBINS];
   for (int b = threadIdx.x; b < NBINS; b += NT) h[b] = 0u;
   __syncthreads();
