@@ -55,8 +55,9 @@ constexpr int TG = RG_TG;            // threads per worker group
 constexpr int TILE_NNZ = RG_TILE_NNZ;    // nonzeros per tile
 constexpr int TILE_ROWS = RG_TILE_ROWS;  // rows per tile
 #ifndef RG_GRAPH_TBUF
-// ring depth of the graph engine's standalone tile kernel: 2 buffers fit 6 blocks (48 tile
-// warps) per SM where 3 fit 4 — more consumer warps is what the sparse passes need
+// ring depth of the graph engine's standalone tile kernel: with 2 buffers shared memory
+// admits 6 blocks per SM where 3 admit 4 (registers then cap pass N at 5: 40-48 tile warps)
+// — more consumer warps is what the sparse passes need
 // (C5c: graph engine 129 -> 135 it/s, C5m +6 %; profiles/r2/ab_engine_c5.jsonl)
 #define RG_GRAPH_TBUF 2
 #endif

@@ -755,8 +755,8 @@ rgdbek_status ensure_graph(rgdbek_ctx* h) {
 // Persistent engine: geometry, buffers and the kernel argument block.
 rgdbek_status setup_persistent(rgdbek_ctx* h) {
   // Engine: the persistent kernel, except for a large sparse system on one GPU, where the
-  // graph engine's standalone tile kernels (2-deep rings, 6 blocks = 48 tile warps per SM
-  // against the persistent kernel's 32) outweigh its ~14 launches per iteration:
+  // graph engine's standalone tile kernels (2-deep rings, 5-6 blocks = 40-48 tile warps per
+  // SM against the persistent kernel's 32) outweigh its ~14 launches per iteration:
   // nnz >= 2^26 (C5c 119.7 -> 135.3 it/s, C5m 1148 -> 1196; C3 / C4 lose 9 % and stay
   // persistent; profiles/r2/ab_engine_c5.jsonl).  A feature only the persistent kernels
   // implement switches back (prefer_persistent).  RGDBEK_ENGINE = graph | persistent.
