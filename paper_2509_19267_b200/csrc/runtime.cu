@@ -67,7 +67,8 @@ struct rgdbek_ctx {
   long long* tilepT = nullptr;          // same for the CSC tiles
   int* tilesT = nullptr;                // CSC row tiles, [ntilesT + 1]
   int ntilesN = 0, ntilesT = 0;
-  int tile_grid = 1;                    // resident 256-thread tile blocks
+  int tile_grid = 1;                    // resident 256-thread tile blocks (pass N kernel)
+  int tile_grid_t = 1;                  // same for the pass T kernel (fewer registers)
   int passN_grid = MAXBLK;              // dense pass N: resident blocks (occupancy x SMs)
   int nCH = 0, nQ = 1;                  // dense pass N: column chunk width, chunks per row
   double* npart = nullptr;              // dense pass N chunk partials [Q][m_loc][2]
@@ -530,7 +531,7 @@ void launch_passT(rgdbek_ctx* h) {
     k_dense_passT<PT_TPB><<<grid, PT_TPB, 2 * h->R * sizeof(double), h->stream>>>(
         h->A, h->lda, (int)h->m_loc, (int)h->n, h->R, h->z, h->xi, h->part, h->st);
   } else {
-    k_csr_tiles<1><<<std::min((h->ntilesT + NT / TG - 1) / (NT / TG), h->tile_grid), NT,
+    k_csr_tiles<1><<<std::min((h->ntilesT + NT / TG - 1) / (NT / TG), h->tile_grid_t), NT,
                      (NT / TG) * sizeof(TileSmemT<GRAPH_TBUF>), h->stream>>>(
         h->cp, h->ri, h->rv, h->tilesT, h->tilepT, h->ntilesT, h->z, h->xi, nullptr, h->s, h->v, h->st,
         h->trace, h->bpart, h->vecT);
@@ -1523,6 +1524,12 @@ rgdbek_status rgdbek_create_csr(rgdbek_handle* out, int64_t m, int64_t n, int64_
     cudaFuncSetAttribute(k_csr_tiles<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_tiles<0>, NT, tsm);
     h->tile_grid = std::max(1, std::min(MAXBLK, nsm * std::max(occ, 1)));
+    // the pass-T kernel needs fewer registers (40 vs 48): its own occupancy (6 blocks per SM
+    // against 5) gives it 48 tile warps per SM — C5c +1.0 %, C5m +1.8 %, standalone pass T
+    // on C5m +4.5 % (profiles/r2/ab_tile_grid_t.log)
+    int occ_t = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, k_csr_tiles<1>, NT, tsm);
+    h->tile_grid_t = std::max(1, std::min(MAXBLK, nsm * std::max(occ_t, 1)));
   }
   clk.mark(h->stream, "tiles T");
   if ((s = finish_create(h)) != RGDBEK_OK) return create_fail(h, s);
